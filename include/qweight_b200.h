@@ -1,0 +1,194 @@
+/*
+ * qweight_b200.h -- C-ABI boundary of the B200 quantized-linear path.
+ *
+ * The reference (arXiv 2311.16442 artifact, `qweight`) exposes its hot path as
+ * a C++ library API in namespace qweight; it has no FFI.  This header is the
+ * thin extern "C" layer the north star asks for: plain pointers and sizes, no
+ * torch or STL types, integer status codes instead of exceptions.  Each entry
+ * point names the reference interface it replaces (paths are relative to the
+ * reference tree, proj/...).
+ *
+ * Device entry points are asynchronous on the caller's stream; *_host entry
+ * points are synchronous and take host buffers.  No entry point falls back to
+ * a CPU implementation: a missing or failing device is reported as
+ * QW_ERR_CUDA.
+ */
+#ifndef QWEIGHT_B200_H
+#define QWEIGHT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QW_ABI_VERSION 1
+
+/* Status codes.  The reference throws qweight::Error (types.hpp:11-14) for
+ * every failure; the C++ shim (qweight_b200.hpp) maps codes back to it. */
+enum qw_status {
+  QW_OK = 0,
+  QW_ERR_ARG = 1,         /* bad argument: length mismatch, null, non-finite
+                             activation (engine.cpp:126-130), workers == 0
+                             (engine.cpp:187-188) */
+  QW_ERR_LAYER = 2,       /* validate_layer failed (bitpack.cpp:212-247) */
+  QW_ERR_CUDA = 3,        /* CUDA runtime / launch failure, no device */
+  QW_ERR_NCCL = 4,        /* collective failure */
+  QW_ERR_UNSUPPORTED = 5, /* geometry outside what the kernels stage */
+  QW_ERR_NOMEM = 6,
+  QW_ERR_IO = 7,          /* container file I/O (container.cpp:89-110) */
+  QW_ERR_FORMAT = 8       /* container corrupt (container.cpp:361-436) */
+};
+
+/* Borrowed, read-only view of a reference PackedLayer (bitpack.hpp:112-124).
+ * Scalars mirror LayerConfig (bitpack.hpp:59-98); sorder / fourbit are passed
+ * as structure-of-arrays because the reference structs are padded
+ * (SorderParam: zero2@0 scale2@2; FourBitParam: scale@0 zero@2, sizeof 4).
+ * All *_len fields are element counts.  The view is only read during the
+ * call that receives it. */
+typedef struct qw_layer_view {
+  uint16_t n, n2, group1, group2, tile;
+  uint32_t rows, cols, n4, pad2, outlier_count;
+  float alpha, outlier_ratio;
+
+  const uint8_t* plan_bits;   /* ChannelPlan.bits, cols entries (plan.hpp:37) */
+  uint64_t plan_bits_len;
+  const uint32_t* plan_perm;  /* ChannelPlan.perm, padded_cols (plan.hpp:38) */
+  uint64_t plan_perm_len;
+
+  const uint8_t* main;        /* rows x paired x 16 */
+  uint64_t main_len;
+  const uint8_t* tail2;       /* rows x tail2_blocks x 12 */
+  uint64_t tail2_len;
+  const uint8_t* tail4;       /* rows x tail4_blocks x 4 */
+  uint64_t tail4_len;
+  const uint8_t* secondary;   /* rows x blocks4 x 4 */
+  uint64_t secondary_len;
+  const uint16_t* meta;       /* rows x triples */
+  uint64_t meta_len;
+  const uint8_t* sorder_zero2;   /* row_blocks x groups_per_row */
+  const uint16_t* sorder_scale2; /* fp16 bits, same count */
+  uint64_t sorder_len;
+  const uint16_t* fourbit_scale; /* fp16 bits, rows x blocks4 */
+  const uint8_t* fourbit_zero;   /* same count */
+  uint64_t fourbit_len;
+  const uint32_t* csr_row_ptr;   /* rows + 1 (outliers.hpp:16-22) */
+  uint64_t csr_row_ptr_len;
+  const uint16_t* csr_col_ind;   /* nnz, permuted 2-bit columns */
+  const uint16_t* csr_values;    /* nnz, fp16 bits */
+  uint64_t csr_nnz;
+} qw_layer_view;
+
+/* Geometry + byte accounting of a layer. */
+typedef struct qw_layer_info {
+  uint32_t rows, cols, padded_cols, n2_padded, n4;
+  uint32_t triples, blocks4, groups, group2, row_blocks;
+  uint32_t quads;            /* 4-row device records */
+  uint32_t quad_bytes;       /* dense bytes of one device record */
+  uint64_t nnz;
+  uint64_t payload_bytes;    /* reference payload_bytes (container.cpp:466-471) */
+  uint64_t device_bytes;     /* bytes the device format occupies in HBM */
+  uint64_t stream_bytes;     /* bytes one matvec reads from the weight format */
+} qw_layer_info;
+
+/* ------------------------------------------------------------------ errors */
+const char* qw_strerror(int status);
+/* Thread-local detail message of the last failing call on this thread. */
+const char* qw_last_error(void);
+int qw_abi_version(void);
+
+/* --------------------------------------------------- host layer (producer)
+ * The reference's producer side (quantizer.hpp:21-34, bitpack.hpp:126-127,
+ * synth.hpp, container.hpp) restated natively so the B200 framework can make
+ * and persist its own inputs.  Results are bit-identical to the reference. */
+typedef struct qw_host_layer qw_host_layer;
+
+/* quantize_layer (quantizer.hpp:21-22 / quantizer.cpp:132-146).
+ * w: rows x cols row-major fp32; h: cols calibration norms.
+ * threads: worker threads for the per-row passes (0 = hardware default). */
+int qw_host_quantize(const float* w, uint32_t rows, uint32_t cols,
+                     const float* h, double alpha, uint32_t group2,
+                     double outlier_ratio, uint32_t threads,
+                     qw_host_layer** out);
+/* Copy + validate_layer a borrowed view into an owning host layer. */
+int qw_host_from_view(const qw_layer_view* view, qw_host_layer** out);
+/* Borrowed view of an owning host layer (valid until qw_host_free). */
+int qw_host_view(const qw_host_layer* layer, qw_layer_view* view);
+void qw_host_free(qw_host_layer* layer);
+/* QWL1 container (container.hpp:50-58). */
+int qw_host_write(const qw_host_layer* layer, const char* path);
+int qw_host_read(const char* path, qw_host_layer** out);
+/* Row shard [r0, r1) (column-parallel TP split; r0, r1 multiples of group2
+ * except r1 == rows) and tile shard [t0, t1) (row-parallel TP split over
+ * paired tiles).  Shards are themselves valid layers. */
+int qw_host_shard_rows(const qw_host_layer* layer, uint32_t r0, uint32_t r1,
+                       qw_host_layer** out);
+int qw_host_shard_tiles(const qw_host_layer* layer, uint32_t t0, uint32_t t1,
+                        qw_host_layer** out, uint32_t* col_offsets /* [4]:
+                        2-bit slot lo, hi, 4-bit slot lo, hi in the parent's
+                        permuted space */);
+
+/* validate_layer (bitpack.cpp:212-247) on a view. */
+int qw_validate_layer(const qw_layer_view* view);
+/* payload_bytes (container.cpp:466-471). */
+uint64_t qw_payload_bytes(const qw_layer_view* view);
+int qw_layer_view_info(const qw_layer_view* view, qw_layer_info* info);
+
+/* synth.hpp:12-22 */
+int qw_synth_gaussian(uint32_t rows, uint32_t cols, uint64_t seed, float* out);
+int qw_plant_outliers(float* w, uint64_t count, double ratio, float scale,
+                      uint64_t seed);
+int qw_synth_calibration(uint32_t cols, uint64_t seed, float* out);
+int qw_synth_activation(uint32_t cols, uint64_t seed, float* out);
+
+/* ------------------------------------------------------- device layer (B200)
+ * Upload: validate_layer, repack into the 4-row device records (DESIGN.md
+ * "HBM layout"), copy to HBM.  The handle is immutable and may be used
+ * concurrently from several streams, each with its own workspace. */
+typedef struct qw_layer qw_layer;
+typedef struct qw_workspace qw_workspace;
+
+int qw_layer_upload(const qw_layer_view* view, int device, qw_layer** out);
+int qw_layer_free(qw_layer* layer);
+int qw_layer_get_info(const qw_layer* layer, qw_layer_info* info);
+
+/* Scratch for one stream: activation prologue buffers for up to max_batch
+ * columns of up to max_cols channels. */
+int qw_workspace_create(int device, uint32_t max_cols, uint32_t max_batch,
+                        qw_workspace** out);
+int qw_workspace_free(qw_workspace* ws);
+
+/* matvec_oracle / matvec_pipelined (engine.hpp:31-36), batched.
+ * x: device fp32 [batch][cols] in ORIGINAL channel order.
+ * y: device fp32 [batch][rows].  stream: cudaStream_t (NULL = legacy).
+ * batch 1..16.  Asynchronous; activations are not checked for finiteness
+ * here (use qw_matvec_host for the reference's checked semantics). */
+int qw_matvec(const qw_layer* layer, const float* x, uint32_t batch, float* y,
+              qw_workspace* ws, void* stream);
+/* Same, launched with programmatic dependent launch so the weight stream of
+ * this call starts before the previous kernel on the stream finishes. */
+int qw_matvec_pdl(const qw_layer* layer, const float* x, uint32_t batch,
+                  float* y, qw_workspace* ws, void* stream);
+/* Host-buffer, synchronous, checked: length and finiteness as the reference
+ * (engine.cpp:124-132).  x_len must equal batch * cols. */
+int qw_matvec_host(const qw_layer* layer, const float* x, uint64_t x_len,
+                   uint32_t batch, float* y, qw_workspace* ws, void* stream);
+
+/* reconstruct_dense (engine.hpp:26): w device fp32 [rows][padded_cols],
+ * permuted order, bit-exact with the reference. */
+int qw_dequant(const qw_layer* layer, float* w, void* stream);
+/* unpack_layer (bitpack.hpp:128): device u8 outputs
+ * codes2 [rows][n2_padded], zeros2 [rows][groups_per_row],
+ * scodes [rows][groups_per_row], codes4 [rows][n4]. */
+int qw_unpack(const qw_layer* layer, uint8_t* codes2, uint8_t* zeros2,
+              uint8_t* scodes, uint8_t* codes4, void* stream);
+
+/* Number of kernels the last qw_matvec* call on this thread launched. */
+int qw_launches_per_matvec(const qw_layer* layer, uint32_t batch);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* QWEIGHT_B200_H */

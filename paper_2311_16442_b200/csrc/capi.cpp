@@ -1,0 +1,612 @@
+// capi.cpp -- extern "C" implementation of include/qweight_b200.h.
+//
+// Converts between the borrowed qw_layer_view and the host PackedLayer,
+// repacks a validated layer into the 4-row device records (qw_device.hpp),
+// owns device memory, and maps every failure to a status code plus a
+// thread-local message.  Nothing here computes y on the CPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/qweight_b200.h"
+#include "device/qw_device.hpp"
+#include "host/qwb_host.hpp"
+
+struct qw_host_layer {
+  qwb::PackedLayer L;
+  // structure-of-arrays mirrors for views
+  std::vector<uint8_t> sorder_zero2, fourbit_zero;
+  std::vector<uint16_t> sorder_scale2, fourbit_scale;
+  void refresh_soa() {
+    sorder_zero2.resize(L.sorder.size());
+    sorder_scale2.resize(L.sorder.size());
+    for (size_t i = 0; i < L.sorder.size(); ++i)
+      sorder_zero2[i] = L.sorder[i].zero2, sorder_scale2[i] = L.sorder[i].scale2;
+    fourbit_zero.resize(L.fourbit.size());
+    fourbit_scale.resize(L.fourbit.size());
+    for (size_t i = 0; i < L.fourbit.size(); ++i)
+      fourbit_zero[i] = L.fourbit[i].zero, fourbit_scale[i] = L.fourbit[i].scale;
+  }
+};
+
+struct qw_layer {
+  qwdev::DeviceLayer dev;
+  int device = 0;
+  int num_sms = 148;
+  qw_layer_info info{};
+};
+
+struct qw_workspace {
+  qwdev::Workspace ws;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& what) {
+  g_last_error = what;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(QW_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& fn) {
+  try {
+    return fn();
+  } catch (const qwb::Error& e) {
+    const std::string m = e.what();
+    const bool layer = m.rfind("layer", 0) == 0 || m.rfind("plan", 0) == 0 || m.rfind("csr", 0) == 0;
+    const bool format = m.rfind("container", 0) == 0;
+    return fail(format ? QW_ERR_FORMAT : (layer ? QW_ERR_LAYER : QW_ERR_ARG), m);
+  } catch (const std::bad_alloc&) {
+    return fail(QW_ERR_NOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(QW_ERR_ARG, e.what());
+  }
+}
+
+template <class T>
+void take(std::vector<T>& dst, const T* src, uint64_t n, const char* name) {
+  if (n && !src) throw qwb::Error(std::string("view: null pointer for ") + name);
+  dst.assign(src, src + n);
+}
+
+qwb::PackedLayer from_view(const qw_layer_view& v) {
+  qwb::PackedLayer L;
+  auto& c = L.cfg;
+  c.n = v.n, c.n2 = v.n2, c.group1 = v.group1, c.group2 = v.group2, c.tile = v.tile;
+  c.rows = v.rows, c.cols = v.cols, c.n4 = v.n4, c.pad2 = v.pad2;
+  c.outlier_count = v.outlier_count, c.alpha = v.alpha, c.outlier_ratio = v.outlier_ratio;
+  L.plan.in_channels = v.cols, L.plan.n4 = v.n4, L.plan.pad2 = v.pad2;
+  take(L.plan.bits, v.plan_bits, v.plan_bits_len, "plan_bits");
+  take(L.plan.perm, v.plan_perm, v.plan_perm_len, "plan_perm");
+  take(L.main, v.main, v.main_len, "main");
+  take(L.tail2, v.tail2, v.tail2_len, "tail2");
+  take(L.tail4, v.tail4, v.tail4_len, "tail4");
+  take(L.secondary, v.secondary, v.secondary_len, "secondary");
+  take(L.meta, v.meta, v.meta_len, "meta");
+  if (v.sorder_len && (!v.sorder_zero2 || !v.sorder_scale2)) throw qwb::Error("view: null sorder");
+  L.sorder.resize(v.sorder_len);
+  for (uint64_t i = 0; i < v.sorder_len; ++i) L.sorder[i] = {v.sorder_zero2[i], v.sorder_scale2[i]};
+  if (v.fourbit_len && (!v.fourbit_zero || !v.fourbit_scale)) throw qwb::Error("view: null fourbit");
+  L.fourbit.resize(v.fourbit_len);
+  for (uint64_t i = 0; i < v.fourbit_len; ++i) L.fourbit[i] = {v.fourbit_scale[i], v.fourbit_zero[i]};
+  take(L.csr.row_ptr, v.csr_row_ptr, v.csr_row_ptr_len, "csr_row_ptr");
+  take(L.csr.col_ind, v.csr_col_ind, v.csr_nnz, "csr_col_ind");
+  take(L.csr.values, v.csr_values, v.csr_nnz, "csr_values");
+  return L;
+}
+
+void fill_view(const qw_host_layer& h, qw_layer_view* v) {
+  const auto& L = h.L;
+  const auto& c = L.cfg;
+  std::memset(v, 0, sizeof *v);
+  v->n = c.n, v->n2 = c.n2, v->group1 = c.group1, v->group2 = c.group2, v->tile = c.tile;
+  v->rows = c.rows, v->cols = c.cols, v->n4 = c.n4, v->pad2 = c.pad2;
+  v->outlier_count = c.outlier_count, v->alpha = c.alpha, v->outlier_ratio = c.outlier_ratio;
+  v->plan_bits = L.plan.bits.data(), v->plan_bits_len = L.plan.bits.size();
+  v->plan_perm = L.plan.perm.data(), v->plan_perm_len = L.plan.perm.size();
+  v->main = L.main.data(), v->main_len = L.main.size();
+  v->tail2 = L.tail2.data(), v->tail2_len = L.tail2.size();
+  v->tail4 = L.tail4.data(), v->tail4_len = L.tail4.size();
+  v->secondary = L.secondary.data(), v->secondary_len = L.secondary.size();
+  v->meta = L.meta.data(), v->meta_len = L.meta.size();
+  v->sorder_zero2 = h.sorder_zero2.data(), v->sorder_scale2 = h.sorder_scale2.data();
+  v->sorder_len = L.sorder.size();
+  v->fourbit_scale = h.fourbit_scale.data(), v->fourbit_zero = h.fourbit_zero.data();
+  v->fourbit_len = L.fourbit.size();
+  v->csr_row_ptr = L.csr.row_ptr.data(), v->csr_row_ptr_len = L.csr.row_ptr.size();
+  v->csr_col_ind = L.csr.col_ind.data(), v->csr_values = L.csr.values.data();
+  v->csr_nnz = L.csr.col_ind.size();
+}
+
+qwdev::Geometry geometry_of(const qwb::LayerConfig& c, uint64_t nnz) {
+  qwdev::Geometry g{};
+  g.rows = c.rows, g.cols = c.cols, g.padded_cols = c.padded_cols();
+  g.n2p = c.n2_padded(), g.n4 = c.n4;
+  g.T2 = c.triples(), g.T4 = c.blocks4(), g.G2 = 3 * g.T2, g.G = g.G2 + g.T4;
+  g.G2s = (g.G2 + 3u) & ~3u;
+  g.group2 = c.group2, g.row_blocks = c.row_blocks();
+  g.quads = (c.rows + qwdev::kRowsPerQuad - 1) / qwdev::kRowsPerQuad;
+  auto a16 = [](uint32_t v) { return (v + 15u) & ~15u; };
+  g.off_c4 = 16u * g.G2;
+  g.off_meta = g.off_c4 + 32u * g.T4;
+  g.off_s4 = g.off_meta + a16(8u * g.T2);
+  g.off_z4 = g.off_s4 + a16(8u * g.T4);
+  g.dense_bytes = g.off_z4 + a16(2u * g.T4);
+  uint32_t mx = 1;
+  for (uint32_t q = 0; q < g.quads; ++q) {
+    const uint32_t r0 = q * 4, r1 = std::min(r0 + 4, c.rows) - 1;
+    mx = std::max(mx, r1 / c.group2 - r0 / c.group2 + 1);
+    if (c.group2 % 4 == 0) break;
+  }
+  g.max_rb_per_quad = mx;
+  g.nnz = nnz;
+  return g;
+}
+
+void fill_info(const qwb::LayerConfig& c, uint64_t nnz, qw_layer_info* info) {
+  const qwdev::Geometry g = geometry_of(c, nnz);
+  std::memset(info, 0, sizeof *info);
+  info->rows = c.rows, info->cols = c.cols, info->padded_cols = c.padded_cols();
+  info->n2_padded = c.n2_padded(), info->n4 = c.n4, info->triples = c.triples();
+  info->blocks4 = c.blocks4(), info->groups = g.G, info->group2 = c.group2;
+  info->row_blocks = c.row_blocks(), info->quads = g.quads, info->quad_bytes = g.dense_bytes;
+  info->nnz = nnz;
+  info->payload_bytes = qwb::payload_bytes(c, nnz);
+  const uint64_t sorder = (uint64_t)g.row_blocks * g.G2s * 4;
+  info->device_bytes = (uint64_t)g.quads * g.dense_bytes + sorder + (uint64_t)g.padded_cols * 4 +
+                       ((uint64_t)c.rows + 1) * 4 + nnz * 4;
+  // one matvec streams every quad record, the sorder rows of each quad, the
+  // quads' row_ptr words and the fused CSR entries
+  uint64_t sorder_reads = 0;
+  for (uint32_t q = 0; q < g.quads; ++q) {
+    const uint32_t r0 = q * 4, r1 = std::min(r0 + 4, c.rows) - 1;
+    sorder_reads += (uint64_t)(r1 / c.group2 - r0 / c.group2 + 1) * g.G2s * 4;
+  }
+  info->stream_bytes = (uint64_t)g.quads * g.dense_bytes + std::min(sorder_reads, sorder) +
+                       ((uint64_t)c.rows + 1) * 4 + nnz * 4;
+}
+
+// Reference stream accessors (bitpack.cpp:175-210) for one row.
+struct RowSrc {
+  const qwb::PackedLayer& L;
+  uint32_t code2_word(uint32_t r, uint32_t g) const {  // 16 codes of 2-bit group g
+    const auto& c = L.cfg;
+    const uint32_t t = g / 3, sub = g % 3, P = c.paired();
+    const uint8_t* b = t < P ? &L.main[((size_t)r * P + t) * 16]
+                             : &L.tail2[((size_t)r * c.tail2_blocks() + (t - P)) * 12];
+    uint32_t w;
+    std::memcpy(&w, b + 4 * sub, 4);
+    return w;
+  }
+  uint32_t code4_word(uint32_t r, uint32_t b, uint32_t half) const {
+    const auto& c = L.cfg;
+    const uint32_t P = c.paired();
+    const uint8_t* p;
+    if (half == 0)
+      p = b < P ? &L.main[((size_t)r * P + b) * 16 + 12]
+                : &L.tail4[((size_t)r * c.tail4_blocks() + (b - P)) * 4];
+    else
+      p = &L.secondary[((size_t)r * c.blocks4() + b) * 4];
+    uint32_t w;
+    std::memcpy(&w, p, 4);
+    return w;
+  }
+};
+
+// North-star (a): the aligned device format.
+void repack(const qwb::PackedLayer& L, const qwdev::Geometry& g, std::vector<uint8_t>& quads,
+            std::vector<uint32_t>& sorder, std::vector<uint32_t>& csr) {
+  const auto& c = L.cfg;
+  quads.assign((size_t)g.quads * g.dense_bytes, 0);
+  RowSrc src{L};
+  for (uint32_t q = 0; q < g.quads; ++q) {
+    uint8_t* rec = &quads[(size_t)q * g.dense_bytes];
+    for (uint32_t i = 0; i < 4; ++i) {
+      const uint32_t r = q * 4 + i;
+      if (r >= c.rows) break;
+      for (uint32_t gi = 0; gi < g.G2; ++gi) {
+        const uint32_t w = src.code2_word(r, gi);
+        std::memcpy(rec + 16 * gi + 4 * i, &w, 4);
+      }
+      for (uint32_t b = 0; b < g.T4; ++b) {
+        const uint32_t w0 = src.code4_word(r, b, 0), w1 = src.code4_word(r, b, 1);
+        std::memcpy(rec + g.off_c4 + 32 * b + 4 * i, &w0, 4);
+        std::memcpy(rec + g.off_c4 + 32 * b + 16 + 4 * i, &w1, 4);
+        const auto& fb = L.fourbit[(size_t)r * g.T4 + b];
+        std::memcpy(rec + g.off_s4 + 8 * b + 2 * i, &fb.scale, 2);
+        uint16_t z4;
+        std::memcpy(&z4, rec + g.off_z4 + 2 * b, 2);
+        z4 = (uint16_t)(z4 | ((fb.zero & 15u) << (4 * i)));
+        std::memcpy(rec + g.off_z4 + 2 * b, &z4, 2);
+      }
+      for (uint32_t t = 0; t < g.T2; ++t)
+        std::memcpy(rec + g.off_meta + 8 * t + 2 * i, &L.meta[(size_t)r * g.T2 + t], 2);
+    }
+  }
+  sorder.assign((size_t)g.row_blocks * g.G2s, 0);
+  for (uint32_t rb = 0; rb < g.row_blocks; ++rb)
+    for (uint32_t j = 0; j < g.G2; ++j) {
+      const auto& p = L.sorder[(size_t)rb * g.G2 + j];
+      sorder[(size_t)rb * g.G2s + j] = (uint32_t)p.scale2 | ((uint32_t)p.zero2 << 16);
+    }
+  csr.resize(L.csr.col_ind.size());
+  for (size_t e = 0; e < csr.size(); ++e)
+    csr[e] = (uint32_t)L.csr.col_ind[e] | ((uint32_t)L.csr.values[e] << 16);
+}
+
+template <class T>
+cudaError_t upload(T** dst, const std::vector<T>& src, size_t min_elems = 1) {
+  const size_t n = std::max(src.size(), min_elems);
+  cudaError_t e = cudaMalloc((void**)dst, n * sizeof(T));
+  if (e != cudaSuccess) return e;
+  if (!src.empty()) e = cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+void free_dev(qwdev::DeviceLayer& d) {
+  cudaFree(d.quads), cudaFree(d.sorder), cudaFree(d.perm), cudaFree(d.row_ptr), cudaFree(d.csr);
+  d = qwdev::DeviceLayer{};
+}
+
+int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
+  if (!L || !ws) return fail(QW_ERR_ARG, "matvec: null layer or workspace");
+  if (batch == 0 || batch > 16) return fail(QW_ERR_ARG, "matvec: batch must be in 1..16");
+  if (batch > ws->ws.max_batch) return fail(QW_ERR_ARG, "matvec: batch exceeds workspace");
+  if (L->dev.g.padded_cols > ws->ws.max_cols)
+    return fail(QW_ERR_ARG, "matvec: layer wider than workspace max_cols");
+  if (L->device != ws->ws.device) return fail(QW_ERR_ARG, "matvec: layer and workspace on different devices");
+  return QW_OK;
+}
+
+int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_workspace* ws,
+               void* stream, bool pdl) {
+  if (int s = check_ws(L, ws, batch)) return s;
+  if (!x || !y) return fail(QW_ERR_ARG, "matvec: null activation or output");
+  int dev_now = -1;
+  cudaGetDevice(&dev_now);
+  if (dev_now != L->device) {
+    cudaError_t e = cudaSetDevice(L->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  }
+  int e = qwdev::launch_prologue(L->dev, x, batch, ws->ws, stream, pdl);
+  if (e) return cuda_fail((cudaError_t)e, "prologue launch");
+  e = qwdev::launch_gemv(L->dev, batch, y, ws->ws, stream, pdl, L->num_sms);
+  if (e) return cuda_fail((cudaError_t)e, "gemv launch");
+  return QW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qw_abi_version(void) { return QW_ABI_VERSION; }
+
+const char* qw_strerror(int s) {
+  switch (s) {
+    case QW_OK: return "ok";
+    case QW_ERR_ARG: return "invalid argument";
+    case QW_ERR_LAYER: return "invalid layer";
+    case QW_ERR_CUDA: return "CUDA error";
+    case QW_ERR_NCCL: return "NCCL error";
+    case QW_ERR_UNSUPPORTED: return "unsupported geometry";
+    case QW_ERR_NOMEM: return "out of memory";
+    case QW_ERR_IO: return "I/O error";
+    case QW_ERR_FORMAT: return "corrupt container";
+    default: return "unknown status";
+  }
+}
+
+const char* qw_last_error(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------------ host
+int qw_host_quantize(const float* w, uint32_t rows, uint32_t cols, const float* h, double alpha,
+                     uint32_t group2, double ratio, uint32_t threads, qw_host_layer** out) {
+  return guarded([&] {
+    if (!w || !h || !out) return fail(QW_ERR_ARG, "quantize: null argument");
+    qwb::WeightMatrix W;
+    W.rows = rows, W.cols = cols;
+    W.data.assign(w, w + (size_t)rows * cols);
+    qwb::QuantizeParams p;
+    p.alpha = alpha, p.group2 = group2, p.outlier_ratio = ratio;
+    auto H = std::make_unique<qw_host_layer>();
+    H->L = qwb::quantize_layer(W, {h, cols}, p, threads);
+    H->refresh_soa();
+    *out = H.release();
+    return (int)QW_OK;
+  });
+}
+
+int qw_host_from_view(const qw_layer_view* v, qw_host_layer** out) {
+  return guarded([&] {
+    if (!v || !out) return fail(QW_ERR_ARG, "from_view: null argument");
+    auto H = std::make_unique<qw_host_layer>();
+    H->L = from_view(*v);
+    qwb::validate_layer(H->L);
+    H->refresh_soa();
+    *out = H.release();
+    return (int)QW_OK;
+  });
+}
+
+int qw_host_view(const qw_host_layer* h, qw_layer_view* v) {
+  if (!h || !v) return fail(QW_ERR_ARG, "view: null argument");
+  fill_view(*h, v);
+  return QW_OK;
+}
+
+void qw_host_free(qw_host_layer* h) { delete h; }
+
+int qw_host_write(const qw_host_layer* h, const char* path) {
+  return guarded([&] {
+    if (!h || !path) return fail(QW_ERR_ARG, "write: null argument");
+    const std::vector<uint8_t> bytes = qwb::serialize_layer(h->L);
+    std::ofstream f(path, std::ios::binary | std::ios::trunc);
+    if (!f) return fail(QW_ERR_IO, std::string("cannot open ") + path + " for writing");
+    f.write((const char*)bytes.data(), (std::streamsize)bytes.size());
+    if (!f) return fail(QW_ERR_IO, std::string("failed to write ") + path);
+    return (int)QW_OK;
+  });
+}
+
+int qw_host_read(const char* path, qw_host_layer** out) {
+  return guarded([&] {
+    if (!path || !out) return fail(QW_ERR_ARG, "read: null argument");
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return fail(QW_ERR_IO, std::string("cannot open ") + path);
+    std::vector<uint8_t> bytes((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    auto H = std::make_unique<qw_host_layer>();
+    H->L = qwb::deserialize_layer(bytes);
+    H->refresh_soa();
+    *out = H.release();
+    return (int)QW_OK;
+  });
+}
+
+int qw_host_shard_rows(const qw_host_layer* h, uint32_t r0, uint32_t r1, qw_host_layer** out) {
+  return guarded([&] {
+    if (!h || !out) return fail(QW_ERR_ARG, "shard_rows: null argument");
+    auto H = std::make_unique<qw_host_layer>();
+    H->L = qwb::shard_rows(h->L, r0, r1);
+    H->refresh_soa();
+    *out = H.release();
+    return (int)QW_OK;
+  });
+}
+
+int qw_host_shard_tiles(const qw_host_layer* h, uint32_t t0, uint32_t t1, qw_host_layer** out,
+                        uint32_t* offs) {
+  return guarded([&] {
+    if (!h || !out) return fail(QW_ERR_ARG, "shard_tiles: null argument");
+    auto H = std::make_unique<qw_host_layer>();
+    H->L = qwb::shard_tiles(h->L, t0, t1);
+    H->refresh_soa();
+    if (offs) {
+      const auto& c = h->L.cfg;
+      offs[0] = 48 * t0;
+      offs[1] = std::min(48 * t1, c.cols - c.n4);
+      offs[2] = c.n2_padded() + 16 * t0;
+      offs[3] = c.n2_padded() + 16 * t1;
+    }
+    *out = H.release();
+    return (int)QW_OK;
+  });
+}
+
+int qw_validate_layer(const qw_layer_view* v) {
+  return guarded([&] {
+    if (!v) return fail(QW_ERR_ARG, "validate: null view");
+    qwb::validate_layer(from_view(*v));
+    return (int)QW_OK;
+  });
+}
+
+uint64_t qw_payload_bytes(const qw_layer_view* v) {
+  if (!v) return 0;
+  qwb::LayerConfig c;
+  c.rows = v->rows, c.cols = v->cols, c.n4 = v->n4, c.pad2 = v->pad2, c.group2 = v->group2;
+  return qwb::payload_bytes(c, v->csr_nnz);
+}
+
+int qw_layer_view_info(const qw_layer_view* v, qw_layer_info* info) {
+  return guarded([&] {
+    if (!v || !info) return fail(QW_ERR_ARG, "info: null argument");
+    qwb::LayerConfig c;
+    c.rows = v->rows, c.cols = v->cols, c.n4 = v->n4, c.pad2 = v->pad2, c.group2 = v->group2;
+    if (c.group2 == 0 || c.rows == 0) return fail(QW_ERR_LAYER, "info: malformed config");
+    fill_info(c, v->csr_nnz, info);
+    return (int)QW_OK;
+  });
+}
+
+int qw_synth_gaussian(uint32_t rows, uint32_t cols, uint64_t seed, float* out) {
+  return guarded([&] {
+    if (!out) return fail(QW_ERR_ARG, "synth: null output");
+    const qwb::WeightMatrix w = qwb::synth_gaussian(rows, cols, seed);
+    std::memcpy(out, w.data.data(), w.data.size() * 4);
+    return (int)QW_OK;
+  });
+}
+
+int qw_plant_outliers(float* w, uint64_t count, double ratio, float scale, uint64_t seed) {
+  return guarded([&] {
+    if (!w && count) return fail(QW_ERR_ARG, "plant: null weights");
+    qwb::plant_outliers({w, count}, ratio, scale, seed);
+    return (int)QW_OK;
+  });
+}
+
+int qw_synth_calibration(uint32_t cols, uint64_t seed, float* out) {
+  return guarded([&] {
+    if (!out) return fail(QW_ERR_ARG, "synth: null output");
+    const auto h = qwb::synth_calibration(cols, seed);
+    std::memcpy(out, h.data(), h.size() * 4);
+    return (int)QW_OK;
+  });
+}
+
+int qw_synth_activation(uint32_t cols, uint64_t seed, float* out) {
+  return guarded([&] {
+    if (!out) return fail(QW_ERR_ARG, "synth: null output");
+    const auto x = qwb::synth_activation(cols, seed);
+    std::memcpy(out, x.data(), x.size() * 4);
+    return (int)QW_OK;
+  });
+}
+
+// ------------------------------------------------------------------ device
+int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
+  return guarded([&] {
+    if (!v || !out) return fail(QW_ERR_ARG, "upload: null argument");
+    const qwb::PackedLayer L = from_view(*v);
+    qwb::validate_layer(L);
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) return fail(QW_ERR_CUDA, "upload: no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(QW_ERR_ARG, "upload: device index out of range");
+    if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    auto H = std::make_unique<qw_layer>();
+    H->device = device;
+    cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, device);
+    H->dev.g = geometry_of(L.cfg, L.csr.nnz());
+    fill_info(L.cfg, L.csr.nnz(), &H->info);
+    std::vector<uint8_t> quads;
+    std::vector<uint32_t> sorder, csr;
+    repack(L, H->dev.g, quads, sorder, csr);
+    if ((e = upload(&H->dev.quads, quads)) != cudaSuccess ||
+        (e = upload(&H->dev.sorder, sorder)) != cudaSuccess ||
+        (e = upload(&H->dev.perm, L.plan.perm)) != cudaSuccess ||
+        (e = upload(&H->dev.row_ptr, L.csr.row_ptr)) != cudaSuccess ||
+        (e = upload(&H->dev.csr, csr)) != cudaSuccess) {
+      free_dev(H->dev);
+      return cuda_fail(e, "upload");
+    }
+    *out = H.release();
+    return (int)QW_OK;
+  });
+}
+
+int qw_layer_free(qw_layer* L) {
+  if (!L) return QW_OK;
+  cudaSetDevice(L->device);
+  free_dev(L->dev);
+  delete L;
+  return QW_OK;
+}
+
+int qw_layer_get_info(const qw_layer* L, qw_layer_info* info) {
+  if (!L || !info) return fail(QW_ERR_ARG, "info: null argument");
+  *info = L->info;
+  return QW_OK;
+}
+
+int qw_workspace_create(int device, uint32_t max_cols, uint32_t max_batch, qw_workspace** out) {
+  if (!out || max_batch == 0 || max_batch > 16 || max_cols == 0)
+    return fail(QW_ERR_ARG, "workspace: bad arguments");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(QW_ERR_CUDA, "workspace: no CUDA device available");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  auto W = std::make_unique<qw_workspace>();
+  auto& ws = W->ws;
+  ws.device = device;
+  ws.max_cols = max_cols + 48;  // room for 2-bit pads
+  ws.max_batch = max_batch;
+  const uint32_t groups = (ws.max_cols + 15) / 16;
+  ws.block_stride = (qwdev::XprepLayout{groups}.block_bytes() + 127u) & ~127u;
+  ws.xp_stride = (ws.max_cols + 31u) & ~31u;
+  if ((e = cudaMalloc((void**)&ws.xprep, (size_t)ws.block_stride * max_batch)) != cudaSuccess ||
+      (e = cudaMalloc((void**)&ws.xp, (size_t)ws.xp_stride * max_batch * 4)) != cudaSuccess ||
+      (e = cudaMalloc((void**)&ws.flags, 16)) != cudaSuccess) {
+    cudaFree(ws.xprep), cudaFree(ws.xp), cudaFree(ws.flags);
+    return cuda_fail(e, "workspace alloc");
+  }
+  cudaMemset(ws.flags, 0, 16);
+  *out = W.release();
+  return QW_OK;
+}
+
+int qw_workspace_free(qw_workspace* W) {
+  if (!W) return QW_OK;
+  cudaSetDevice(W->ws.device);
+  cudaFree(W->ws.xprep), cudaFree(W->ws.xp), cudaFree(W->ws.flags);
+  delete W;
+  return QW_OK;
+}
+
+int qw_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_workspace* ws,
+              void* stream) {
+  return run_matvec(L, x, batch, y, ws, stream, false);
+}
+
+int qw_matvec_pdl(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_workspace* ws,
+                  void* stream) {
+  return run_matvec(L, x, batch, y, ws, stream, true);
+}
+
+int qw_matvec_host(const qw_layer* L, const float* x, uint64_t x_len, uint32_t batch, float* y,
+                   qw_workspace* ws, void* stream) {
+  if (int s = check_ws(L, ws, batch)) return s;
+  if (!x || !y) return fail(QW_ERR_ARG, "matvec: null activation or output");
+  // checked_permute (engine.cpp:124-132)
+  if (x_len != (uint64_t)batch * L->info.cols)
+    return fail(QW_ERR_ARG, "matvec: activation length != input channels");
+  for (uint64_t i = 0; i < x_len; ++i)
+    if (!std::isfinite(x[i])) return fail(QW_ERR_ARG, "matvec: non-finite activation");
+  cudaSetDevice(L->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  float *dx = nullptr, *dy = nullptr;
+  const size_t xb = x_len * 4, yb = (size_t)batch * L->info.rows * 4;
+  cudaError_t e;
+  if ((e = cudaMallocAsync((void**)&dx, xb, st)) != cudaSuccess) return cuda_fail(e, "alloc x");
+  if ((e = cudaMallocAsync((void**)&dy, yb, st)) != cudaSuccess) {
+    cudaFreeAsync(dx, st);
+    return cuda_fail(e, "alloc y");
+  }
+  int status = QW_OK;
+  if ((e = cudaMemcpyAsync(dx, x, xb, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    status = cuda_fail(e, "copy x");
+  if (!status) status = run_matvec(L, dx, batch, dy, ws, stream, false);
+  if (!status && (e = cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    status = cuda_fail(e, "copy y");
+  cudaFreeAsync(dx, st);
+  cudaFreeAsync(dy, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess && !status) status = cuda_fail(e, "sync");
+  return status;
+}
+
+int qw_dequant(const qw_layer* L, float* w, void* stream) {
+  if (!L || !w) return fail(QW_ERR_ARG, "dequant: null argument");
+  cudaSetDevice(L->device);
+  const int e = qwdev::launch_dequant(L->dev, w, stream);
+  return e ? cuda_fail((cudaError_t)e, "dequant launch") : QW_OK;
+}
+
+int qw_unpack(const qw_layer* L, uint8_t* codes2, uint8_t* zeros2, uint8_t* scodes, uint8_t* codes4,
+              void* stream) {
+  if (!L || ((!codes2 || !zeros2 || !scodes) && L->dev.g.G2) || (!codes4 && L->dev.g.n4))
+    return fail(QW_ERR_ARG, "unpack: null argument");
+  cudaSetDevice(L->device);
+  const int e = qwdev::launch_unpack(L->dev, codes2, zeros2, scodes, codes4, stream);
+  return e ? cuda_fail((cudaError_t)e, "unpack launch") : QW_OK;
+}
+
+int qw_launches_per_matvec(const qw_layer* L, uint32_t batch) {
+  (void)L;
+  return 1 + (int)batch;
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+"""B200 engine: device-resident layers and the quantized linear forward.
+
+Mirrors the reference engine API (engine.hpp:19-70) on the GPU:
+
+  reference                          here
+  ---------------------------------  ------------------------------------------
+  reconstruct_dense(layer)           DeviceLayer.reconstruct_dense()  (bit-exact)
+  unpack_layer(layer)                DeviceLayer.unpack()             (bit-exact)
+  matvec_oracle / matvec_pipelined   DeviceLayer.matvec(x)           (1e-2 rel)
+  MatvecResult{y, stage_ns, wall_ns} matvec_checked(x) -> MatvecResult
+
+PyTorch only supplies device memory and streams; every kernel is ours
+(libqweight_b200.so).  A missing GPU raises QWeightError -- there is no CPU
+path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._native import LayerInfo, QWeightError, check, lib
+from .layer import PackedLayer
+
+try:  # torch is plumbing (device buffers, streams, events)
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+def _stream_handle(stream=None) -> int:
+    if torch is None:
+        return 0
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Workspace:
+    """Per-stream activation scratch (qw_workspace_create)."""
+
+    def __init__(self, device: int = 0, max_cols: int = 65536, max_batch: int = 16):
+        self.device = device
+        self.max_cols, self.max_batch = max_cols, max_batch
+        self._h = C.c_void_p()
+        check(lib().qw_workspace_create(device, max_cols, max_batch, C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib().qw_workspace_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ws: dict = {}
+
+
+def default_workspace(device: int) -> Workspace:
+    ws = _default_ws.get(device)
+    if ws is None:
+        ws = _default_ws[device] = Workspace(device)
+    return ws
+
+
+@dataclass
+class MatvecResult:
+    """MatvecResult (engine.hpp:19-23): y plus timing.  stage_ns holds the
+    device time of the fused kernel in slot 3 (there are no separate stages
+    on the GPU: fetch/scale/decode/FMA are one kernel)."""
+    y: np.ndarray
+    stage_ns: list = field(default_factory=lambda: [0, 0, 0, 0])
+    wall_ns: int = 0
+
+
+class DeviceLayer:
+    """A packed layer uploaded to HBM in the 4-row device format."""
+
+    def __init__(self, layer: PackedLayer, device: int = 0):
+        self.layer_cfg = layer.cfg
+        self.device = device
+        self._h = C.c_void_p()
+        check(lib().qw_layer_upload(C.byref(layer.view()), device, C.byref(self._h)))
+        inf = LayerInfo()
+        check(lib().qw_layer_get_info(self._h, C.byref(inf)))
+        self.info = inf.as_dict()
+
+    @property
+    def rows(self): return self.info["rows"]
+    @property
+    def cols(self): return self.info["cols"]
+    @property
+    def padded_cols(self): return self.info["padded_cols"]
+
+    def close(self):
+        if self._h:
+            lib().qw_layer_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- forward
+    def matvec(self, x, out=None, workspace: Workspace | None = None, stream=None,
+               pdl: bool = False):
+        """y = W_q x on the GPU.  x: torch cuda fp32 [cols] or [batch, cols]
+        in original channel order.  Returns fp32 [rows] / [batch, rows]."""
+        if torch is None:
+            raise QWeightError(3, "torch is required for device tensors")
+        squeeze = x.dim() == 1
+        xb = x.reshape(1, -1) if squeeze else x
+        if xb.dtype != torch.float32 or not xb.is_cuda or not xb.is_contiguous():
+            raise QWeightError(1, "matvec: x must be a contiguous cuda float32 tensor")
+        batch = xb.shape[0]
+        if xb.shape[1] != self.cols:
+            raise QWeightError(1, "matvec: activation length != input channels")
+        if out is None:
+            out = torch.empty((batch, self.rows), dtype=torch.float32, device=xb.device)
+        ws = workspace or default_workspace(self.device)
+        fn = lib().qw_matvec_pdl if pdl else lib().qw_matvec
+        check(fn(self._h, C.c_void_p(xb.data_ptr()), batch, C.c_void_p(out.data_ptr()), ws._h,
+                 C.c_void_p(_stream_handle(stream))))
+        return out.reshape(-1) if squeeze else out
+
+    def matvec_checked(self, x: np.ndarray, workspace: Workspace | None = None) -> MatvecResult:
+        """Host buffers in and out, with the reference's activation checks
+        (engine.cpp:124-132): wrong length or a non-finite value raises."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        batch = 1 if x.ndim == 1 else x.shape[0]
+        y = np.empty((batch, self.rows), dtype=np.float32)
+        ws = workspace or default_workspace(self.device)
+        t0 = time.perf_counter_ns()
+        check(lib().qw_matvec_host(self._h, x.ctypes.data, x.size, batch, y.ctypes.data, ws._h,
+                                   C.c_void_p(_stream_handle())))
+        wall = time.perf_counter_ns() - t0
+        return MatvecResult(y=y.reshape(-1) if x.ndim == 1 else y, wall_ns=wall,
+                            stage_ns=[0, 0, 0, wall])
+
+    # ------------------------------------------------------------ bit-exact
+    def reconstruct_dense(self, stream=None):
+        """reconstruct_dense (engine.hpp:26): rows x padded_cols fp32, permuted."""
+        w = torch.empty((self.rows, self.padded_cols), dtype=torch.float32,
+                        device=f"cuda:{self.device}")
+        check(lib().qw_dequant(self._h, C.c_void_p(w.data_ptr()), C.c_void_p(_stream_handle(stream))))
+        return w
+
+    def unpack(self, stream=None) -> dict:
+        """unpack_layer codes (bitpack.hpp:128): codes2, zeros2, scodes, codes4."""
+        inf, dev = self.info, f"cuda:{self.device}"
+        gpr = 3 * inf["triples"]
+        codes2 = torch.empty((self.rows, max(inf["n2_padded"], 1)), dtype=torch.uint8, device=dev)
+        zeros2 = torch.empty((self.rows, max(gpr, 1)), dtype=torch.uint8, device=dev)
+        scodes = torch.empty((self.rows, max(gpr, 1)), dtype=torch.uint8, device=dev)
+        codes4 = torch.empty((self.rows, max(inf["n4"], 1)), dtype=torch.uint8, device=dev)
+        check(lib().qw_unpack(self._h, C.c_void_p(codes2.data_ptr()), C.c_void_p(zeros2.data_ptr()),
+                              C.c_void_p(scodes.data_ptr()), C.c_void_p(codes4.data_ptr()),
+                              C.c_void_p(_stream_handle(stream))))
+        return {"codes2": codes2[:, :inf["n2_padded"]], "zeros2": zeros2[:, :gpr],
+                "scodes": scodes[:, :gpr], "codes4": codes4[:, :inf["n4"]]}
+
+    def launches_per_matvec(self, batch: int = 1) -> int:
+        return int(lib().qw_launches_per_matvec(self._h, batch))
+
+
+def upload(layer: PackedLayer, device: int = 0) -> DeviceLayer:
+    return DeviceLayer(layer, device)

@@ -1,0 +1,167 @@
+"""GPU parity: the sm_100a path against the C oracle (and through it the
+reference) on identical inputs.
+
+  * K0 unpack and K1 dequant are bit-exact (reference unpack_layer /
+    reconstruct_dense), pads and outlier slots included.
+  * K2+K3 matvec y matches matvec_reference_f64 within the north-star
+    tolerance: rel-L2 <= 1e-2 and max-abs <= 1e-2 * max|y| (fp16 partial
+    sums; typically ~5e-4).
+Edge cases follow the reference tests: tails (T2 != T4), pads, pure 2-bit /
+pure 4-bit layers, rows not a multiple of 4, odd group2, zero x, no
+outliers, dense outliers, random zero2 (helpers.hpp random_groups).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2311_16442_b200 as qw
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def rel_l2(y, ref):
+    ref = np.asarray(ref, np.float64)
+    den = np.linalg.norm(ref)
+    return float(np.linalg.norm(np.asarray(y, np.float64) - ref) / (den if den else 1.0))
+
+
+def check_layer(layer, x, device=0):
+    torch = _torch()
+    dl = qw.DeviceLayer(layer, device)
+    # K1: bit-exact reconstruct_dense
+    w = dl.reconstruct_dense().cpu().numpy()
+    ref_w = oracle.reconstruct_dense(layer)
+    assert np.array_equal(w.view(np.uint32), ref_w.view(np.uint32))
+    # K0: bit-exact unpack_layer
+    got = {k: v.cpu().numpy() for k, v in dl.unpack().items()}
+    ref = oracle.unpack(layer)
+    for k in ref:
+        assert np.array_equal(got[k], ref[k]), k
+    # K2/K3: y within tolerance of the f64 oracle
+    y = dl.matvec(torch.from_numpy(np.ascontiguousarray(x)).cuda()).cpu().numpy()
+    ref_y = oracle.matvec_f64(layer, x)
+    assert np.all(np.isfinite(y))
+    err = rel_l2(y, ref_y)
+    assert err <= TOL, err
+    scale = np.max(np.abs(ref_y)) if ref_y.size else 0.0
+    assert np.max(np.abs(y - ref_y)) <= TOL * max(scale, 1e-30) + 1e-30
+    return err, dl
+
+
+GEOMS = [
+    # rows, cols, alpha, group2, ratio
+    (20, 80, 0.25, 16, 0.002),     # pads + tails (test_engine.cpp:51-60)
+    (24, 160, 0.5, 16, 0.005),     # tail4-heavy
+    (9, 96, 0.0, 16, 0.0),         # pure 2-bit, rows % 4 != 0
+    (9, 96, 1.0, 16, 0.0),         # pure 4-bit
+    (37, 160, 0.25, 16, 0.01),     # odd rows, dense outliers
+    (64, 512, 0.25, 5, 0.01),      # group2 not a multiple of 4
+    (130, 1024, 0.25, 128, 0.002), # g2 = 128 (config 1 "group 128")
+    (16, 1024, 0.25, 16, 0.0),     # zero outliers (test_engine.cpp:71-76)
+]
+
+
+@pytest.mark.parametrize("rows,cols,alpha,g2,ratio", GEOMS)
+def test_geometries(rows, cols, alpha, g2, ratio):
+    layer = qw.synth_layer(rows, cols, seed=rows * 31 + cols, alpha=alpha, group2=g2,
+                           outlier_ratio=ratio)
+    x = qw.synth_activation(cols, rows + 100)
+    check_layer(layer, x)
+
+
+def test_zero_activation_gives_zero():
+    torch = _torch()
+    layer = qw.synth_layer(12, 64, seed=10)
+    dl = qw.DeviceLayer(layer)
+    y = dl.matvec(torch.zeros(64, device="cuda")).cpu().numpy()
+    assert np.all(y == 0.0)
+
+
+def test_random_groups_with_nonzero_zero2():
+    """helpers.hpp random_groups: random codes, zero2 0..15, fp16 scales."""
+    rng = np.random.default_rng(5)
+    base = qw.synth_layer(32, 256, seed=3)
+    c = base.cfg
+    layer = qw.PackedLayer(
+        cfg=c, plan_bits=base.plan_bits, plan_perm=base.plan_perm,
+        main=rng.integers(0, 256, base.main.size, dtype=np.uint8),
+        tail2=rng.integers(0, 256, base.tail2.size, dtype=np.uint8),
+        tail4=rng.integers(0, 256, base.tail4.size, dtype=np.uint8),
+        secondary=rng.integers(0, 256, base.secondary.size, dtype=np.uint8),
+        meta=rng.integers(0, 65536, base.meta.size, dtype=np.uint16),
+        sorder_zero2=rng.integers(0, 16, base.sorder_zero2.size, dtype=np.uint8),
+        # moderate scales keep the fp16 products finite
+        sorder_scale2=np.array([qw_f16(v) for v in rng.uniform(0.01, 0.2, base.sorder_zero2.size)],
+                               np.uint16),
+        fourbit_scale=np.array([qw_f16(v) for v in rng.uniform(0.01, 0.5, base.fourbit_zero.size)],
+                               np.uint16),
+        fourbit_zero=rng.integers(0, 16, base.fourbit_zero.size, dtype=np.uint8),
+        row_ptr=base.row_ptr, col_ind=base.col_ind, values=base.values)
+    qw.validate_layer(layer)
+    x = qw.synth_activation(256, 4)
+    check_layer(layer, x)
+
+
+def qw_f16(v: float) -> int:
+    return int(np.float16(v).view(np.uint16))
+
+
+def test_large_activation_range():
+    """Power-of-two group scaling keeps fp16 partials finite for large x."""
+    layer = qw.synth_layer(64, 512, seed=21)
+    x = qw.synth_activation(512, 22) * np.float32(3e4)
+    x[5] = 1e9
+    err, _ = check_layer(layer, x)
+    assert err < 5e-3
+
+
+def test_batched_columns_match_single():
+    torch = _torch()
+    layer = qw.synth_layer(96, 512, seed=8)
+    dl = qw.DeviceLayer(layer)
+    xs = np.stack([qw.synth_activation(512, 50 + b) for b in range(4)])
+    Y = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
+    for b in range(4):
+        ref = oracle.matvec_f64(layer, xs[b])
+        assert rel_l2(Y[b], ref) <= TOL
+
+
+def test_checked_host_path_validates_activation():
+    layer = qw.synth_layer(8, 64, seed=11)
+    dl = qw.DeviceLayer(layer)
+    with pytest.raises(qw.QWeightError):
+        dl.matvec_checked(np.zeros(63, np.float32))
+    bad = np.ones(64, np.float32)
+    bad[7] = np.nan
+    with pytest.raises(qw.QWeightError):
+        dl.matvec_checked(bad)
+    res = dl.matvec_checked(qw.synth_activation(64, 3))
+    assert rel_l2(res.y, oracle.matvec_f64(layer, qw.synth_activation(64, 3))) <= TOL
+    assert res.wall_ns > 0
+
+
+def test_deterministic_runs():
+    torch = _torch()
+    layer = qw.synth_layer(128, 1024, seed=25)
+    dl = qw.DeviceLayer(layer)
+    x = torch.from_numpy(qw.synth_activation(1024, 26)).cuda()
+    a = dl.matvec(x).cpu().numpy()
+    b = dl.matvec(x).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("rows,cols", [(4096, 4096), (11008, 4096), (4096, 11008)])
+def test_llama7b_shapes(rows, cols):
+    """Config 2 shapes at full size: bit-exact dequant + y tolerance."""
+    layer = qw.synth_layer(rows, cols, seed=7)
+    x = qw.synth_activation(cols, 8)
+    err, _ = check_layer(layer, x)
+    assert err < 2e-3
