@@ -1,0 +1,381 @@
+#!/usr/bin/env python3
+"""bench.py -- batch-1 Llama-2-7B decode GEMVs through the B200 quantized linear.
+
+Workload (BASELINE.json configs[1]): every Llama-2-7B linear shape -- q, k, v,
+o (4096x4096), gate, up (11008x4096), down (4096x11008) -- as mixed 2/4-bit +
+fp16-outlier layers (alpha 0.25, g1 16, g2 16, 0.2 % outliers), one batch-1
+GEMV each, for every one of the model's 32 decoder layers: one "step" is one
+token's worth of linears (224 GEMVs, 2.2 GB of packed weights, > 17x the L2).
+Weights are quantized from synthetic N(0,1) matrices (reference synth /
+quantize_layer recipe, bit-identical producer); the 7 distinct layers are
+cloned device-to-device so each of the 224 GEMVs reads its own HBM copy.
+
+  metric  : achieved HBM GB/s = algorithmic bytes / time (BASELINE.md §2:
+            B_alg = payload_bytes + 4*(IC + OC) per GEMV), with us/layer
+  value   : device-resident inputs, CUDA-graph replay of the step
+  e2e     : through LinearStack.run (public API): pinned H2D of all
+            activations + step + D2H of all outputs, host wall clock
+  roofline: the fused GEMV kernel alone on the q/k/v/o shape
+  cpu_baseline: the reference's matvec_pipelined (oracle/_ref, all host
+            threads) on one decoder layer's 7 linears (bounded sample)
+
+`--impl reference` times the reference CPU implementation (oracle/_ref) on
+the same 7 linears.  Under torchrun every rank runs its own replica of the
+step (batch-1 decode does not shard without a collective): scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "µs/layer and achieved HBM GB/s (% of roofline), batch-1 Llama-2-7B GEMV"
+SHAPES_7B = [("q_proj", 4096, 4096), ("k_proj", 4096, 4096), ("v_proj", 4096, 4096),
+             ("o_proj", 4096, 4096), ("gate_proj", 11008, 4096), ("up_proj", 11008, 4096),
+             ("down_proj", 4096, 11008)]
+ALPHA, GROUP2, RATIO = 0.25, 16, 0.002
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def b_alg(payload: int, rows: int, cols: int, batch: int = 1) -> int:
+    """payload_bytes + 4*b*IC + 4*b*OC."""
+    return payload + 4 * batch * (rows + cols)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.out = index, None, None
+
+    def __enter__(self):
+        try:
+            self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.out, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if self.proc is None or self.out is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        rows = []
+        for line in Path(self.out.name).read_text().splitlines():
+            f = [c.strip() for c in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- layers
+def make_layers(rank: int, world: int, cache_dir: Path, threads: int):
+    """Quantize the 7 distinct linears once (rank 0), share through QWL1 files."""
+    import paper_2311_16442_b200 as qw
+    paths = [cache_dir / f"{name}.qwl" for name, _, _ in SHAPES_7B]
+    if rank == 0:
+        for i, (name, rows, cols) in enumerate(SHAPES_7B):
+            if not paths[i].exists():
+                layer = qw.synth_layer(rows, cols, seed=7 + i, alpha=ALPHA, group2=GROUP2,
+                                       outlier_ratio=RATIO, threads=threads)
+                qw.write_packed_layer(layer, str(paths[i]) + ".tmp")
+                os.replace(str(paths[i]) + ".tmp", paths[i])
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    return [qw.read_packed_layer(str(p)) for p in paths]
+
+
+# --------------------------------------------------------------- CPU legs
+def cpu_reference_sample(layers, budget_s: float, threads: int):
+    """The reference's own matvec_pipelined (or the C port) on the 7 linears."""
+    import oracle
+    import paper_2311_16442_b200 as qw
+    xs = [qw.synth_activation(L.cfg.cols, 8 + i) for i, L in enumerate(layers)]
+    total = sum(b_alg(qw.payload_bytes(L), L.cfg.rows, L.cfg.cols) for L in layers)
+    if oracle.ref_available():
+        refs = [oracle.RefLayer.from_layer(L) for L in layers]
+        kind, run = "reference", (lambda: [r.matvec_pipelined(x, threads)[1] for r, x in zip(refs, xs)])
+        cores = threads
+    else:
+        kind, cores = "port", 1
+
+        def run():
+            out = []
+            for L, x in zip(layers, xs):
+                t0 = time.perf_counter_ns()
+                oracle.matvec_oracle(L, x)
+                out.append(time.perf_counter_ns() - t0)
+            return out
+    run()  # warm caches (bench_matvec does the same, engine.cpp:332-333)
+    passes, t_start = [], time.perf_counter()
+    while time.perf_counter() - t_start < budget_s or len(passes) < 2:
+        passes.append(sum(run()))
+        if len(passes) >= 50:
+            break
+    best = min(passes)
+    return {"value": total / best, "unit": "GB/s", "cores": cores, "kind": kind,
+            "sample": f"one decoder layer (7 Llama-2-7B linears, {total} B_alg), "
+                      f"{len(passes)} passes, best pass {best / 1e6:.2f} ms "
+                      f"({'matvec_pipelined, workers=' + str(threads) if kind == 'reference' else 'C oracle port, 1 thread'})",
+            "ms_per_pass": best / 1e6, "bytes_per_pass": total}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    threads = os.cpu_count() or 1
+    cache = Path(tempfile.gettempdir()) / "qw_bench_cache"
+    cache.mkdir(exist_ok=True)
+    layers = make_layers(0, 1, cache, threads)
+    import paper_2311_16442_b200 as qw
+    xs = [qw.synth_activation(L.cfg.cols, 8 + i) for i, L in enumerate(layers)]
+    total = sum(b_alg(qw.payload_bytes(L), L.cfg.rows, L.cfg.cols) for L in layers)
+    if oracle.ref_available():
+        kind, cores = "reference", threads
+        refs = [oracle.RefLayer.from_layer(L) for L in layers]
+
+        def step():
+            t0 = time.perf_counter_ns()
+            for r, x in zip(refs, xs):
+                r.matvec_pipelined(x, threads)
+            return time.perf_counter_ns() - t0
+    else:
+        kind, cores = "port", 1
+
+        def step():
+            t0 = time.perf_counter_ns()
+            for L, x in zip(layers, xs):
+                oracle.matvec_oracle(L, x)
+            return time.perf_counter_ns() - t0
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    ms = statistics.mean(times) / 1e6
+    value = total / (ms * 1e6)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "us_per_layer": round(ms * 1e3 / len(layers), 3),
+        "config": {"workload": "llama2-7b linears q/k/v/o 4096x4096, gate/up 11008x4096, "
+                               "down 4096x11008; batch-1 GEMV; one decoder layer per step "
+                               "(bounded CPU sample)",
+                   "alpha": ALPHA, "group1": 16, "group2": GROUP2, "outlier_ratio": RATIO,
+                   "batch": 1},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": kind,
+                         "sample": f"7 linears per step x {args.steps} steps"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import paper_2311_16442_b200 as qw
+    from paper_2311_16442_b200.stack import LinearStack
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    threads = max(1, (os.cpu_count() or 1) // max(world, 1)) if rank else (os.cpu_count() or 1)
+    cache = Path(os.environ.get("QW_BENCH_CACHE", Path(tempfile.gettempdir()) / "qw_bench_cache"))
+    cache.mkdir(parents=True, exist_ok=True)
+    t_prep = time.perf_counter()
+    base = make_layers(rank, world, cache, threads)
+    dls = [qw.DeviceLayer(L, local) for L in base]
+    payload = [qw.payload_bytes(L) for L in base]
+    per_layer = []
+    for l in range(args.layers):
+        for i, dl in enumerate(dls):
+            per_layer.append((i, dl if l == 0 else dl.clone()))
+    stack = LinearStack([d for _, d in per_layer], device=local, batch=1, pdl=not args.no_pdl)
+    x_all = np.concatenate([qw.synth_activation(base[i].cfg.cols, 1000 * l + i)
+                            for l in range(args.layers) for i in range(len(base))])
+    stack.x.copy_(torch.from_numpy(x_all))
+    step_bytes = sum(b_alg(payload[i], base[i].cfg.rows, base[i].cfg.cols) for i, _ in per_layer)
+    n_gemv = len(per_layer)
+    prep_s = time.perf_counter() - t_prep
+
+    # correctness spot check of the captured path before timing
+    stack.capture()
+    stack.replay()
+    torch.cuda.synchronize()
+    if rank == 0:
+        import oracle
+        for j in (0, 4, 6):
+            y = stack.y_of(j).cpu().numpy().reshape(-1)
+            ref = oracle.matvec_f64(base[j], x_all[stack.slots[j].x_off:stack.slots[j].x_off + base[j].cfg.cols])
+            rel = float(np.linalg.norm(y - ref) / np.linalg.norm(ref))
+            assert rel <= 1e-2, f"bench parity check failed on {SHAPES_7B[j][0]}: {rel}"
+
+    def timed(fn, steps, warm):
+        for _ in range(warm):
+            fn()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        if dist is not None:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms
+
+    # ---- headline: device-resident step (graph replay)
+    with ClockSampler(local) as clk:
+        ms_step = timed(stack.replay, args.steps, args.warmup)
+    clocks = clk.summary()
+
+    # ---- dominant kernel alone: fused GEMV on the q/k/v/o shape
+    sel = lambda d: d.rows == 4096 and d.cols == 4096  # noqa: E731
+    g_q = stack.capture_subset(sel)
+    n_q = sum(1 for _, d in per_layer if sel(d))
+    ms_q = timed(g_q.replay, args.steps, args.warmup)
+    q_bytes = b_alg(payload[0], 4096, 4096)
+    us_q = ms_q * 1e3 / n_q
+
+    # ---- e2e through the public API with host buffers
+    e2e_times = []
+    for _ in range(args.warmup):
+        stack.run()
+    if dist is not None:
+        dist.barrier()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        stack.run()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_ms = statistics.mean(e2e_times) * 1e3
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    hbm_peak, peak_kind = peaks()
+    value = world * step_bytes / (ms_step * 1e6)  # GB/s over all ranks
+    achieved_q = q_bytes / (us_q * 1e3)
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    traffic = None
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("gemv_q_proj", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference_sample(base, args.cpu_budget, os.cpu_count() or 1)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp16x2-dot/fp32-accumulate", "data": "synthetic",
+            "us_per_layer": round(ms_step * 1e3 / n_gemv, 4),
+            "pct_of_hbm_roofline": round(100 * value / world / hbm_peak, 2),
+            "config": {"workload": "llama2-7b decode step: q/k/v/o 4096x4096, gate/up 11008x4096, "
+                                   f"down 4096x11008 x {args.layers} layers ({n_gemv} batch-1 GEMVs)",
+                       "alpha": ALPHA, "group1": 16, "group2": GROUP2, "outlier_ratio": RATIO,
+                       "batch": 1, "bytes_per_step": step_bytes,
+                       "l2": "inputs larger than L2 (distinct HBM copy per GEMV)",
+                       "launch": "CUDA graph, programmatic dependent launch" if not args.no_pdl
+                                 else "CUDA graph"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved_q, 2), "peak": hbm_peak,
+                         "unit": "GB/s", "frac": round(achieved_q / hbm_peak, 4),
+                         "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "gemv_kernel (fused dequant GEMV + CSR), q_proj 4096x4096",
+                         "us_per_launch": round(us_q, 4), "algorithmic_bytes": q_bytes},
+            "e2e": {"value": round(world * step_bytes / (e2e_ms * 1e6), 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": stack.h2d_bytes, "d2h_bytes_per_step": stack.d2h_bytes,
+                    "ms_per_step": round(e2e_ms, 4),
+                    "api": "LinearStack.run (pinned H2D, graph, D2H, sync)"},
+            "gpu_launches": n_gemv * args.steps,
+            "clocks": clocks,
+            "prep_s": round(prep_s, 1),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=32, help="decoder layers per step")
+    ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU sample")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

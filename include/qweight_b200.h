@@ -153,8 +153,9 @@ int qw_layer_upload(const qw_layer_view* view, int device, qw_layer** out);
 int qw_layer_free(qw_layer* layer);
 int qw_layer_get_info(const qw_layer* layer, qw_layer_info* info);
 
-/* Scratch for one stream: activation prologue buffers for up to max_batch
- * columns of up to max_cols channels. */
+/* Scratch for one stream (up to max_batch columns of up to max_cols
+ * channels).  The fused batch-1 kernel needs none; kept for the batched
+ * path and the non-finite-activation flag. */
 int qw_workspace_create(int device, uint32_t max_cols, uint32_t max_batch,
                         qw_workspace** out);
 int qw_workspace_free(qw_workspace* ws);
@@ -184,7 +185,21 @@ int qw_dequant(const qw_layer* layer, float* w, void* stream);
 int qw_unpack(const qw_layer* layer, uint8_t* codes2, uint8_t* zeros2,
               uint8_t* scodes, uint8_t* codes4, void* stream);
 
-/* Number of kernels the last qw_matvec* call on this thread launched. */
+/* Device-to-device copy of an uploaded layer (same device). */
+int qw_layer_clone(const qw_layer* layer, qw_layer** out);
+
+/* Diagnostics: one batch-1 matvec that records qw_debug_timeline_events()
+ * clock64 stamps per CTA into device buffer `stamps` (grid x events):
+ * 0 entry, 1 first ring of weight copies issued, 2 all copies issued,
+ * 3 outliers done, 4 all quads reduced, 5 y written, 6 consumer past
+ * griddepcontrol.wait, 7 activation prologue done, 8 first quad present,
+ * 9 consumer done.  repeat > 1 makes the consumers re-run the resident
+ * quads (compute-rate measurement; y is then not meaningful). */
+int qw_debug_timeline(const qw_layer* layer, const float* x, float* y,
+                      unsigned long long* stamps, uint32_t repeat, void* stream);
+int qw_debug_timeline_events(void);
+
+/* Number of kernels one qw_matvec call launches. */
 int qw_launches_per_matvec(const qw_layer* layer, uint32_t batch);
 
 #ifdef __cplusplus

@@ -92,6 +92,10 @@ _SIGS = {
     "qw_dequant": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "qw_unpack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_void_p]),
+    "qw_layer_clone": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "qw_debug_timeline": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
+                                    C.c_void_p]),
+    "qw_debug_timeline_events": (C.c_int, []),
     "qw_launches_per_matvec": (C.c_int, [C.c_void_p, C.c_uint32]),
 }
 

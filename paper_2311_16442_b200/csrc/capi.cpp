@@ -17,6 +17,7 @@
 
 #include "../../include/qweight_b200.h"
 #include "device/qw_device.hpp"
+#include "device/qw_layout.hpp"
 #include "host/qwb_host.hpp"
 
 struct qw_host_layer {
@@ -214,17 +215,30 @@ void repack(const qwb::PackedLayer& L, const qwdev::Geometry& g, std::vector<uin
   RowSrc src{L};
   for (uint32_t q = 0; q < g.quads; ++q) {
     uint8_t* rec = &quads[(size_t)q * g.dense_bytes];
-    for (uint32_t i = 0; i < 4; ++i) {
-      const uint32_t r = q * 4 + i;
-      if (r >= c.rows) break;
-      for (uint32_t gi = 0; gi < g.G2; ++gi) {
-        const uint32_t w = src.code2_word(r, gi);
-        std::memcpy(rec + 16 * gi + 4 * i, &w, 4);
+    // reference words of the quad's rows (rows past the end stay zero)
+    const uint32_t nr = std::min<uint32_t>(4, c.rows - q * 4);
+    for (uint32_t gi = 0; gi < g.G2; ++gi) {
+      uint32_t w[4] = {0, 0, 0, 0};
+      for (uint32_t i = 0; i < nr; ++i) w[i] = src.code2_word(q * 4 + i, gi);
+      uint32_t out[4];
+      qwdev::pack_pair2(w[0], w[1], out);
+      qwdev::pack_pair2(w[2], w[3], out + 2);
+      std::memcpy(rec + 16 * gi, out, 16);
+    }
+    for (uint32_t b = 0; b < g.T4; ++b) {
+      uint32_t lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+      for (uint32_t i = 0; i < nr; ++i) {
+        lo[i] = src.code4_word(q * 4 + i, b, 0);
+        hi[i] = src.code4_word(q * 4 + i, b, 1);
       }
+      uint32_t out[8];
+      qwdev::pack_pair4(lo[0], hi[0], lo[1], hi[1], out);
+      qwdev::pack_pair4(lo[2], hi[2], lo[3], hi[3], out + 4);
+      std::memcpy(rec + g.off_c4 + 32 * b, out, 32);
+    }
+    for (uint32_t i = 0; i < nr; ++i) {
+      const uint32_t r = q * 4 + i;
       for (uint32_t b = 0; b < g.T4; ++b) {
-        const uint32_t w0 = src.code4_word(r, b, 0), w1 = src.code4_word(r, b, 1);
-        std::memcpy(rec + g.off_c4 + 32 * b + 4 * i, &w0, 4);
-        std::memcpy(rec + g.off_c4 + 32 * b + 16 + 4 * i, &w1, 4);
         const auto& fb = L.fourbit[(size_t)r * g.T4 + b];
         std::memcpy(rec + g.off_s4 + 8 * b + 2 * i, &fb.scale, 2);
         uint16_t z4;
@@ -258,6 +272,7 @@ cudaError_t upload(T** dst, const std::vector<T>& src, size_t min_elems = 1) {
 
 void free_dev(qwdev::DeviceLayer& d) {
   cudaFree(d.quads), cudaFree(d.sorder), cudaFree(d.perm), cudaFree(d.row_ptr), cudaFree(d.csr);
+  cudaFree(d.perm16);
   d = qwdev::DeviceLayer{};
 }
 
@@ -281,9 +296,7 @@ int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_w
     cudaError_t e = cudaSetDevice(L->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   }
-  int e = qwdev::launch_prologue(L->dev, x, batch, ws->ws, stream, pdl);
-  if (e) return cuda_fail((cudaError_t)e, "prologue launch");
-  e = qwdev::launch_gemv(L->dev, batch, y, ws->ws, stream, pdl, L->num_sms);
+  const int e = qwdev::launch_gemv(L->dev, x, batch, y, stream, pdl);
   if (e) return cuda_fail((cudaError_t)e, "gemv launch");
   return QW_OK;
 }
@@ -485,11 +498,17 @@ int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
     std::vector<uint8_t> quads;
     std::vector<uint32_t> sorder, csr;
     repack(L, H->dev.g, quads, sorder, csr);
+    std::vector<uint16_t> perm16(L.plan.perm.size());
+    for (size_t i = 0; i < perm16.size(); ++i)
+      perm16[i] = L.plan.perm[i] == qwb::kPad ? 0 : (uint16_t)L.plan.perm[i];
+    if (int pe = qwdev::plan_gemv(H->dev, H->num_sms, L.csr.row_ptr.data()))
+      return cuda_fail((cudaError_t)pe, "gemv plan");
     if ((e = upload(&H->dev.quads, quads)) != cudaSuccess ||
         (e = upload(&H->dev.sorder, sorder)) != cudaSuccess ||
         (e = upload(&H->dev.perm, L.plan.perm)) != cudaSuccess ||
         (e = upload(&H->dev.row_ptr, L.csr.row_ptr)) != cudaSuccess ||
-        (e = upload(&H->dev.csr, csr)) != cudaSuccess) {
+        (e = upload(&H->dev.csr, csr)) != cudaSuccess ||
+        (e = upload(&H->dev.perm16, perm16)) != cudaSuccess) {
       free_dev(H->dev);
       return cuda_fail(e, "upload");
     }
@@ -521,20 +540,11 @@ int qw_workspace_create(int device, uint32_t max_cols, uint32_t max_batch, qw_wo
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   auto W = std::make_unique<qw_workspace>();
-  auto& ws = W->ws;
-  ws.device = device;
-  ws.max_cols = max_cols + 48;  // room for 2-bit pads
-  ws.max_batch = max_batch;
-  const uint32_t groups = (ws.max_cols + 15) / 16;
-  ws.block_stride = (qwdev::XprepLayout{groups}.block_bytes() + 127u) & ~127u;
-  ws.xp_stride = (ws.max_cols + 31u) & ~31u;
-  if ((e = cudaMalloc((void**)&ws.xprep, (size_t)ws.block_stride * max_batch)) != cudaSuccess ||
-      (e = cudaMalloc((void**)&ws.xp, (size_t)ws.xp_stride * max_batch * 4)) != cudaSuccess ||
-      (e = cudaMalloc((void**)&ws.flags, 16)) != cudaSuccess) {
-    cudaFree(ws.xprep), cudaFree(ws.xp), cudaFree(ws.flags);
-    return cuda_fail(e, "workspace alloc");
-  }
-  cudaMemset(ws.flags, 0, 16);
+  W->ws.device = device;
+  W->ws.max_cols = max_cols + 48;  // room for 2-bit pads
+  W->ws.max_batch = max_batch;
+  if ((e = cudaMalloc((void**)&W->ws.flags, 16)) != cudaSuccess) return cuda_fail(e, "workspace alloc");
+  cudaMemset(W->ws.flags, 0, 16);
   *out = W.release();
   return QW_OK;
 }
@@ -542,7 +552,7 @@ int qw_workspace_create(int device, uint32_t max_cols, uint32_t max_batch, qw_wo
 int qw_workspace_free(qw_workspace* W) {
   if (!W) return QW_OK;
   cudaSetDevice(W->ws.device);
-  cudaFree(W->ws.xprep), cudaFree(W->ws.xp), cudaFree(W->ws.flags);
+  cudaFree(W->ws.flags);
   delete W;
   return QW_OK;
 }
@@ -604,9 +614,46 @@ int qw_unpack(const qw_layer* L, uint8_t* codes2, uint8_t* zeros2, uint8_t* scod
   return e ? cuda_fail((cudaError_t)e, "unpack launch") : QW_OK;
 }
 
+int qw_layer_clone(const qw_layer* L, qw_layer** out) {
+  if (!L || !out) return fail(QW_ERR_ARG, "clone: null argument");
+  cudaSetDevice(L->device);
+  auto H = std::make_unique<qw_layer>();
+  H->device = L->device, H->num_sms = L->num_sms, H->info = L->info;
+  H->dev.g = L->dev.g;
+  H->dev.plan = L->dev.plan;
+  const auto& g = L->dev.g;
+  auto dup = [](auto** dst, const auto* src, size_t bytes) {
+    cudaError_t e = cudaMalloc((void**)dst, bytes ? bytes : 4);
+    if (e == cudaSuccess && bytes) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyDeviceToDevice);
+    return e;
+  };
+  cudaError_t e;
+  if ((e = dup(&H->dev.quads, L->dev.quads, (size_t)g.quads * g.dense_bytes)) != cudaSuccess ||
+      (e = dup(&H->dev.sorder, L->dev.sorder, (size_t)g.row_blocks * g.G2s * 4)) != cudaSuccess ||
+      (e = dup(&H->dev.perm, L->dev.perm, (size_t)g.padded_cols * 4)) != cudaSuccess ||
+      (e = dup(&H->dev.row_ptr, L->dev.row_ptr, ((size_t)g.rows + 1) * 4)) != cudaSuccess ||
+      (e = dup(&H->dev.csr, L->dev.csr, (size_t)g.nnz * 4)) != cudaSuccess ||
+      (e = dup(&H->dev.perm16, L->dev.perm16, (size_t)g.padded_cols * 2)) != cudaSuccess) {
+    free_dev(H->dev);
+    return cuda_fail(e, "clone");
+  }
+  *out = H.release();
+  return QW_OK;
+}
+
+int qw_debug_timeline(const qw_layer* L, const float* x, float* y, unsigned long long* stamps,
+                      uint32_t repeat, void* stream) {
+  if (!L || !x || !y || !stamps) return fail(QW_ERR_ARG, "timeline: null argument");
+  cudaSetDevice(L->device);
+  const int e = qwdev::launch_gemv(L->dev, x, 1, y, stream, false, stamps, repeat);
+  return e ? cuda_fail((cudaError_t)e, "gemv launch") : QW_OK;
+}
+
+int qw_debug_timeline_events(void) { return (int)qwdev::kTimelineEvents; }
+
 int qw_launches_per_matvec(const qw_layer* L, uint32_t batch) {
   (void)L;
-  return 1 + (int)batch;
+  return (int)batch;
 }
 
 }  // extern "C"

@@ -37,38 +37,46 @@ struct Geometry {
   uint64_t nnz;
 };
 
+// Launch plan of the fused GEMV, fixed at upload so launches stay
+// capture-safe (no attribute calls on the launch path).
+constexpr uint32_t kMaxGrid = 304;
+
+struct GemvPlan {
+  uint32_t grid = 0;                   // CTAs (persistent, contiguous quad ranges)
+  uint32_t warps = 0, teams = 1, kmax = 0;  // consumer warps, 32-group chunks per warp
+  uint32_t nslot = 0, uq = 2, win = 0;  // slots, quads per slot, quads per reduction window
+  uint32_t nchunks = 0, nq_max = 0, uniform_rb = 0;
+  uint32_t so_off = 0, part_off = 0, xg_off = 0, misc_off = 0, bar_off = 0;  // smem layout
+  uint32_t smem = 0;
+  uint32_t csr_lo[kMaxGrid + 1] = {};  // first CSR entry of each CTA's rows
+};
+
 struct DeviceLayer {
   Geometry g;
+  GemvPlan plan;
   uint8_t* quads = nullptr;      // quads * dense_bytes
   uint32_t* sorder = nullptr;    // row_blocks * G2s
   uint32_t* perm = nullptr;      // padded_cols (0xFFFFFFFF = pad)
+  uint16_t* perm16 = nullptr;    // padded_cols, original channel (pads 0; known by position)
   uint32_t* row_ptr = nullptr;   // rows + 1
   uint32_t* csr = nullptr;       // nnz (col | fp16 << 16)
 };
 
-// Activation prologue output for one column (the "xprep" block): per group
-// 16 fp16 x' in the lane pairing the unpack uses, then sum(x') and the
-// power-of-two unscale factor per group; followed by the permuted fp32 x.
-struct XprepLayout {
-  uint32_t groups;
-  uint32_t xh_bytes() const { return groups * 32u; }
-  uint32_t block_bytes() const { return (groups * 40u + 15u) & ~15u; }  // xh | sx | ex
-};
-
+// Per-stream scratch (kept in the ABI for the batched path; the fused
+// batch-1 kernel needs none).
 struct Workspace {
   int device = 0;
   uint32_t max_cols = 0, max_batch = 0;
-  uint8_t* xprep = nullptr;    // max_batch * block_bytes(max groups)
-  float* xp = nullptr;         // max_batch * max padded cols
-  uint32_t* flags = nullptr;   // non-finite activation flag
-  uint32_t block_stride = 0, xp_stride = 0;
+  uint32_t* flags = nullptr;
 };
 
 // Launchers (return cudaError_t as int).
-int launch_prologue(const DeviceLayer& L, const float* x, uint32_t batch, const Workspace& ws,
-                    void* stream, bool pdl);
-int launch_gemv(const DeviceLayer& L, uint32_t batch, float* y, const Workspace& ws, void* stream,
-                bool pdl, int num_sms);
+// Fill L.plan for a device with num_sms SMs (returns cudaError_t).
+int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr);
+// y[col] = W_q x[col] for col < batch: one fused kernel per column.
+constexpr uint32_t kTimelineEvents = 42;  // 10 phase + 8 x (unit ready, done) + 8 issue + 8 arrival
+int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream,
+                bool pdl, unsigned long long* dbg = nullptr, uint32_t repeat = 1);
 int launch_dequant(const DeviceLayer& L, float* w, void* stream);
 int launch_unpack(const DeviceLayer& L, uint8_t* codes2, uint8_t* zeros2, uint8_t* scodes,
                   uint8_t* codes4, void* stream);

@@ -81,11 +81,14 @@ class MatvecResult:
 class DeviceLayer:
     """A packed layer uploaded to HBM in the 4-row device format."""
 
-    def __init__(self, layer: PackedLayer, device: int = 0):
-        self.layer_cfg = layer.cfg
+    def __init__(self, layer: PackedLayer | None, device: int = 0, _handle=None):
         self.device = device
         self._h = C.c_void_p()
-        check(lib().qw_layer_upload(C.byref(layer.view()), device, C.byref(self._h)))
+        if _handle is not None:
+            self._h = _handle
+        else:
+            self.layer_cfg = layer.cfg
+            check(lib().qw_layer_upload(C.byref(layer.view()), device, C.byref(self._h)))
         inf = LayerInfo()
         check(lib().qw_layer_get_info(self._h, C.byref(inf)))
         self.info = inf.as_dict()
@@ -165,6 +168,14 @@ class DeviceLayer:
                               C.c_void_p(_stream_handle(stream))))
         return {"codes2": codes2[:, :inf["n2_padded"]], "zeros2": zeros2[:, :gpr],
                 "scodes": scodes[:, :gpr], "codes4": codes4[:, :inf["n4"]]}
+
+    def clone(self) -> "DeviceLayer":
+        """Device-to-device copy (distinct HBM buffers, same content)."""
+        h = C.c_void_p()
+        check(lib().qw_layer_clone(self._h, C.byref(h)))
+        out = DeviceLayer(None, self.device, _handle=h)
+        out.layer_cfg = getattr(self, "layer_cfg", None)
+        return out
 
     def launches_per_matvec(self, batch: int = 1) -> int:
         return int(lib().qw_launches_per_matvec(self._h, batch))

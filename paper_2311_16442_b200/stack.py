@@ -1,0 +1,118 @@
+"""LinearStack: a decode step over many quantized linears, captured once.
+
+The reference has no model layer; this is the thinnest runner
+that exercises the hot path the way a decoder does: every linear of every
+layer runs once per token.  All activations live in one device buffer and
+all outputs in another, so a host round trip is two copies; the launches
+(one fused kernel per linear, chained with programmatic dependent launch)
+are captured in one CUDA graph.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .engine import DeviceLayer, Workspace
+
+try:
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+@dataclass
+class _Slot:
+    layer: DeviceLayer
+    x_off: int
+    y_off: int
+
+
+class LinearStack:
+    def __init__(self, layers: list[DeviceLayer], device: int = 0, batch: int = 1,
+                 pdl: bool = True):
+        self.device, self.batch, self.pdl = device, batch, pdl
+        self.dev = torch.device(f"cuda:{device}")
+        xo = yo = 0
+        self.slots = []
+        for dl in layers:
+            self.slots.append(_Slot(dl, xo, yo))
+            xo += batch * dl.cols
+            yo += batch * dl.rows
+        self.x = torch.zeros(xo, dtype=torch.float32, device=self.dev)
+        self.y = torch.zeros(yo, dtype=torch.float32, device=self.dev)
+        self.x_host = torch.zeros(xo, dtype=torch.float32).pin_memory()
+        self.y_host = torch.zeros(yo, dtype=torch.float32).pin_memory()
+        max_cols = max(dl.padded_cols for dl in layers)
+        self.ws = Workspace(device, max_cols, batch)
+        self.graph = None
+        self.gemv_graph = None
+
+    # ------------------------------------------------------------ views
+    def x_of(self, i: int):
+        s = self.slots[i]
+        return self.x[s.x_off:s.x_off + self.batch * s.layer.cols].view(self.batch, s.layer.cols)
+
+    def y_of(self, i: int):
+        s = self.slots[i]
+        return self.y[s.y_off:s.y_off + self.batch * s.layer.rows].view(self.batch, s.layer.rows)
+
+    # ------------------------------------------------------------ launches
+    def launch_step(self, stream=None):
+        for i, s in enumerate(self.slots):
+            s.layer.matvec(self.x_of(i), out=self.y_of(i), workspace=self.ws, stream=stream,
+                           pdl=self.pdl)
+
+    def launch_subset(self, select, stream=None):
+        """Launch only the linears `select(layer)` accepts (kernel-only timing)."""
+        for i, s in enumerate(self.slots):
+            if select(s.layer):
+                s.layer.matvec(self.x_of(i), out=self.y_of(i), workspace=self.ws, stream=stream,
+                               pdl=self.pdl)
+
+    def capture(self):
+        """Capture one decode step into a CUDA graph (after a warm run)."""
+        self.launch_step()
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch_step()
+        torch.cuda.synchronize(self.dev)
+        self.graph = g
+        return g
+
+    def capture_subset(self, select):
+        self.launch_subset(select)
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch_subset(select)
+        torch.cuda.synchronize(self.dev)
+        return g
+
+    def replay(self):
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    # ------------------------------------------------------------ host API
+    def run(self, x_host: np.ndarray | None = None) -> np.ndarray:
+        """One decode step end to end: pinned host -> HBM copy of every
+        activation, the captured step, HBM -> pinned host copy of every
+        output, synchronise.  Returns the outputs (flat, slot order)."""
+        if x_host is not None:
+            self.x_host.numpy()[:] = x_host
+        stream = torch.cuda.current_stream(self.dev)
+        self.x.copy_(self.x_host, non_blocking=True)
+        self.replay()
+        self.y_host.copy_(self.y, non_blocking=True)
+        stream.synchronize()
+        return self.y_host.numpy()
+
+    @property
+    def h2d_bytes(self) -> int:
+        return self.x.numel() * 4
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.y.numel() * 4

@@ -65,6 +65,10 @@ GEOMS = [
     (64, 512, 0.25, 5, 0.01),      # group2 not a multiple of 4
     (130, 1024, 0.25, 128, 0.002), # g2 = 128 (config 1 "group 128")
     (16, 1024, 0.25, 16, 0.0),     # zero outliers (test_engine.cpp:71-76)
+    (40, 512, 0.25, 1, 0.01),      # group2 = 1: every row its own 2-order block
+    (21, 768, 0.25, 3, 0.01),      # group2 = 3
+    (64, 28672, 0.25, 16, 0.002),  # 70B down width: 56 chunks, 4 per warp
+    (16, 40960, 0.25, 16, 0.002),  # 80 chunks: x reloaded per quad
 ]
 
 
