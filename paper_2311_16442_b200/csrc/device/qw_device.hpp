@@ -39,14 +39,14 @@ struct Geometry {
 
 // Launch plan of the fused GEMV, fixed at upload so launches stay
 // capture-safe (no attribute calls on the launch path).
-constexpr uint32_t kMaxGrid = 304;
+constexpr uint32_t kMaxGrid = 448;
 
 struct GemvPlan {
   uint32_t grid = 0;                   // CTAs (persistent, contiguous quad ranges)
-  uint32_t warps = 0, teams = 1, kmax = 0;  // consumer warps, 32-group chunks per warp
+  uint32_t warps = 0, warps2 = 0, teams = 1, kmax = 0;  // consumer warps, 32-group chunks per warp
   uint32_t nslot = 0, uq = 2, win = 0;  // slots, quads per slot, quads per reduction window
-  uint32_t nchunks = 0, nq_max = 0, uniform_rb = 0;
-  uint32_t so_off = 0, part_off = 0, xg_off = 0, misc_off = 0, bar_off = 0;  // smem layout
+  uint32_t nchunks = 0, nq_max = 0, uniform_rb = 0, xsm = 0, rb_magic = 0;
+  uint32_t so_off = 0, part_off = 0, xg_off = 0, misc_off = 0, win_off = 0, bar_off = 0;  // smem layout
   uint32_t smem = 0;
   uint32_t csr_lo[kMaxGrid + 1] = {};  // first CSR entry of each CTA's rows
 };
@@ -74,7 +74,7 @@ struct Workspace {
 // Fill L.plan for a device with num_sms SMs (returns cudaError_t).
 int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr);
 // y[col] = W_q x[col] for col < batch: one fused kernel per column.
-constexpr uint32_t kTimelineEvents = 42;  // 10 phase + 8 x (unit ready, done) + 8 issue + 8 arrival
+constexpr uint32_t kTimelineEvents = 8;  // entry, copies issued, prologue, first quad, consumers, y, csr
 int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream,
                 bool pdl, unsigned long long* dbg = nullptr, uint32_t repeat = 1);
 int launch_dequant(const DeviceLayer& L, float* w, void* stream);

@@ -19,10 +19,8 @@ x = torch.from_numpy(qw.synth_activation(cols, 8)).cuda()
 y = torch.empty(rows, device="cuda")
 E = lib().qw_debug_timeline_events()
 grid = dl.info["quads"] if dl.info["quads"] < 148 else 148
-names = ["entry", "ring issued", "all issued", "csr done", "reduced", "y written",
-         "past pdl wait", "prologue done", "first quad", "consumer done"]
-names += [f"u{i} {w}" for i in range(8) for w in ("ready", "done")]
-names += [f"u{i} issued" for i in range(8)] + [f"u{i} landed" for i in range(8)]
+names = ["entry", "copies issued", "prologue done", "first quad", "consumers done", "y written",
+         "csr done", "-"]
 for trial in range(2):
     st = torch.zeros(grid * E, dtype=torch.int64, device="cuda")
     for _ in range(3):  # warm
@@ -36,7 +34,7 @@ for trial in range(2):
     print(f"trial {trial}: cycles from entry (mean / max over CTAs)")
     if REP > 1:
         nq = dl.info["quads"] / grid
-        span = d[:, 9] - d[:, 8]
+        span = d[:, 4] - d[:, 3]
         print(f"  repeat {REP}: consumer loop {span.mean():.0f} cycles -> {span.mean() / (REP * nq):.1f} cycles/quad")
     for i in np.argsort(d.mean(0)):
         if d[:, i].max() <= 0 or d[:, i].min() < 0: continue
