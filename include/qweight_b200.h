@@ -189,14 +189,17 @@ int qw_unpack(const qw_layer* layer, uint8_t* codes2, uint8_t* zeros2,
 int qw_layer_clone(const qw_layer* layer, qw_layer** out);
 
 /* Diagnostics: one batch-1 matvec that records qw_debug_timeline_events()
- * clock64 stamps per CTA into device buffer `stamps` (grid x events):
- * 0 entry, 1 first ring of weight copies issued, 2 all copies issued,
- * 3 outliers done, 4 all quads reduced, 5 y written, 6 consumer past
- * griddepcontrol.wait, 7 activation prologue done, 8 first quad present,
- * 9 consumer done.  repeat > 1 makes the consumers re-run the resident
- * quads (compute-rate measurement; y is then not meaningful). */
+ * stamps per CTA into device buffer `stamps` (grid x events):
+ * 0 entry, 1 all weight copies issued, 2 activation prologue done,
+ * 3 first unit landed, 4 consumers done, 5 y written, 6 outliers done.
+ * flags: bit 0 = launch with programmatic dependent launch, bit 1 = stamp
+ * %globaltimer (ns, comparable across SMs and kernels) instead of clock64,
+ * bit 2 = x independent of the preceding kernel (no dependency wait).
+ * repeat > 1 makes the consumers re-run the resident quads (compute-rate
+ * measurement; y is then not meaningful). */
 int qw_debug_timeline(const qw_layer* layer, const float* x, float* y,
-                      unsigned long long* stamps, uint32_t repeat, void* stream);
+                      unsigned long long* stamps, uint32_t repeat, uint32_t flags,
+                      void* stream);
 int qw_debug_timeline_events(void);
 
 /* Number of kernels one qw_matvec call launches. */

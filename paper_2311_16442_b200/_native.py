@@ -94,7 +94,7 @@ _SIGS = {
                             C.c_void_p]),
     "qw_layer_clone": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "qw_debug_timeline": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
-                                    C.c_void_p]),
+                                      C.c_uint32, C.c_void_p]),
     "qw_debug_timeline_events": (C.c_int, []),
     "qw_launches_per_matvec": (C.c_int, [C.c_void_p, C.c_uint32]),
 }

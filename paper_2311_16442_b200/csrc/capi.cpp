@@ -501,8 +501,19 @@ int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
     std::vector<uint16_t> perm16(L.plan.perm.size());
     for (size_t i = 0; i < perm16.size(); ++i)
       perm16[i] = L.plan.perm[i] == qwb::kPad ? 0 : (uint16_t)L.plan.perm[i];
-    if (int pe = qwdev::plan_gemv(H->dev, H->num_sms, L.csr.row_ptr.data()))
+    if (int pe = qwdev::plan_gemv(H->dev, H->num_sms, L.csr.row_ptr.data())) {
+      if (pe == (int)cudaErrorInvalidConfiguration)
+        return fail(QW_ERR_UNSUPPORTED, "upload: layer too wide for the fused GEMV (at most 60 "
+                                        "chunks of 32 groups, i.e. about 30720 input channels)");
       return cuda_fail((cudaError_t)pe, "gemv plan");
+    }
+    {  // 2^-P so that 15 * max|scale2| * 2^-P lies in [2^14, 2^15): fp16 1st-order scales
+      float mx = 0.0f;
+      for (const auto& sp : L.sorder) mx = std::max(mx, std::fabs(qwb::f16_to_f32(sp.scale2)));
+      int P = 0;
+      if (mx > 0.0f && std::isfinite(mx)) P = std::ilogb(15.0f * mx) - 14;
+      H->dev.plan.s_scale = std::ldexp(1.0f, -std::max(-100, std::min(100, P)));
+    }
     if ((e = upload(&H->dev.quads, quads)) != cudaSuccess ||
         (e = upload(&H->dev.sorder, sorder)) != cudaSuccess ||
         (e = upload(&H->dev.perm, L.plan.perm)) != cudaSuccess ||
@@ -642,10 +653,11 @@ int qw_layer_clone(const qw_layer* L, qw_layer** out) {
 }
 
 int qw_debug_timeline(const qw_layer* L, const float* x, float* y, unsigned long long* stamps,
-                      uint32_t repeat, void* stream) {
+                      uint32_t repeat, uint32_t flags, void* stream) {
   if (!L || !x || !y || !stamps) return fail(QW_ERR_ARG, "timeline: null argument");
   cudaSetDevice(L->device);
-  const int e = qwdev::launch_gemv(L->dev, x, 1, y, stream, false, stamps, repeat);
+  const int e = qwdev::launch_gemv(L->dev, x, 1, y, stream, flags & 1u, stamps, repeat,
+                                   (flags & 2u) != 0, (flags & 4u) ? qwdev::kXIndependent : 0u);
   return e ? cuda_fail((cudaError_t)e, "gemv launch") : QW_OK;
 }
 

@@ -45,8 +45,9 @@ struct GemvPlan {
   uint32_t grid = 0;                   // CTAs (persistent, contiguous quad ranges)
   uint32_t warps = 0, warps2 = 0, teams = 1, kmax = 0;  // consumer warps, 32-group chunks per warp
   uint32_t nslot = 0, uq = 2, win = 0;  // slots, quads per slot, quads per reduction window
-  uint32_t nchunks = 0, nq_max = 0, uniform_rb = 0, xsm = 0, rb_magic = 0;
-  uint32_t so_off = 0, part_off = 0, xg_off = 0, misc_off = 0, win_off = 0, bar_off = 0;  // smem layout
+  uint32_t nchunks = 0, nq_max = 0, uniform_rb = 0, xsm = 0, rb_magic = 0, rb_one = 0;
+  float s_scale = 1.0f;  // 2^-P applied to 2-bit s1 so 15 * max scale2 * 2^-P fits fp16
+  uint32_t so_off = 0, part_off = 0, xg_off = 0, misc_off = 0, win_off = 0, pre_off = 0, bar_off = 0;  // smem layout
   uint32_t smem = 0;
   uint32_t csr_lo[kMaxGrid + 1] = {};  // first CSR entry of each CTA's rows
 };
@@ -74,9 +75,13 @@ struct Workspace {
 // Fill L.plan for a device with num_sms SMs (returns cudaError_t).
 int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr);
 // y[col] = W_q x[col] for col < batch: one fused kernel per column.
-constexpr uint32_t kTimelineEvents = 8;  // entry, copies issued, prologue, first quad, consumers, y, csr
+constexpr uint32_t kTimelineEvents = 12;  // entry, copies issued, prologue, first quad, consumers, y, csr
+// flags: kXIndependent = x was not written by the preceding kernel on the
+// stream (skip the programmatic-dependency wait before reading it)
+constexpr uint32_t kXIndependent = 2u;
 int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream,
-                bool pdl, unsigned long long* dbg = nullptr, uint32_t repeat = 1);
+                bool pdl, unsigned long long* dbg = nullptr, uint32_t repeat = 1,
+                bool global_clock = false, uint32_t flags = 0);
 int launch_dequant(const DeviceLayer& L, float* w, void* stream);
 int launch_unpack(const DeviceLayer& L, uint8_t* codes2, uint8_t* zeros2, uint8_t* scodes,
                   uint8_t* codes4, void* stream);

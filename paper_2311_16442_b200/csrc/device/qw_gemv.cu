@@ -119,41 +119,27 @@ __device__ __forceinline__ half2 dot4(uint4 w, const half2* X) {
   return __hadd2(a, b);
 }
 
-// ------------------------------------------------------------ prologue
-// One lane's 16-channel group: x'_k = x_k 2^-sh with max|x'| in [2^10, 2^11)
-// (so sum|x'| < 2^15 stays inside fp16 for the zero-point term), stored as
-// X[k] = fp16(x'_k 2^-bitpos(k)) duplicated into both halves.
-struct XPrep {
-  float nsx;  // -sum x'_k 2^-24 (of the fp16-rounded x')
-  float ex;   // 2^(sh + 24): product units -> x units
-};
-
-// 2^e as the product of two normal floats (|e| <= 252)
-__device__ __forceinline__ float scale2pow(float v, int e) {
-  const int e1 = max(-126, min(127, e));
-  return v * pow2f(e1) * pow2f(max(-126, min(127, e - e1)));
+// ------------------------------------------------------------ helpers
+// acc += float(a) * float(b) for fp16 halves, one rounding (sm_100 mixed FMA)
+__device__ __forceinline__ float fhfma_lo(half2 a, half2 b, float c) {
+  float d;
+  asm("{.reg .b16 al, ah, bl, bh;\n\tmov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+      "fma.rn.f32.f16 %0, al, bl, %3;}"
+      : "=f"(d)
+      : "r"(*reinterpret_cast<uint32_t*>(&a)), "r"(*reinterpret_cast<uint32_t*>(&b)), "f"(c));
+  return d;
 }
-
-// v: the group's 16 activations in permuted order (pads already 0).
-__device__ __forceinline__ XPrep prepare_group(half2* X, const float* v, bool two) {
-  float m = 0.0f;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) m = fmaxf(m, fabsf(v[k]));
-  const int eb = (int)((__float_as_uint(m) >> 23) & 0xFFu);
-  // floor(log2 m) for normal m; subnormal and zero groups use the smallest exponent
-  const int sh = (eb == 0 ? -126 : eb - 127) - 10;
-  float sx = 0.0f;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int b = two ? 2 * (k & 3) : 4 * (k & 1);
-    const __half h = __float2half_rn(scale2pow(v[k], -sh - b));
-    X[k] = __half2half2(h);
-    sx += __half2float(h) * pow2f(b - 24);
-  }
-  XPrep p;
-  p.nsx = -sx;
-  p.ex = pow2f(max(-126, min(127, sh + 24)));
-  return p;
+__device__ __forceinline__ float fhfma_hi(half2 a, half2 b, float c) {
+  float d;
+  asm("{.reg .b16 al, ah, bl, bh;\n\tmov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+      "fma.rn.f32.f16 %0, ah, bh, %3;}"
+      : "=f"(d)
+      : "r"(*reinterpret_cast<uint32_t*>(&a)), "r"(*reinterpret_cast<uint32_t*>(&b)), "f"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t pack_h2(float2 v) {  // cvt.rn.f16x2.f32
+  const half2 h = __float22half2_rn(v);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 
 // ------------------------------------------------------------ K2+K3 GEMV
@@ -166,25 +152,42 @@ struct GemvArgs {
   const float* x;
   float* y;
   Geometry g;
-  uint32_t W, W2, S, grid, nq_max, rb_magic;  // rb = umulhi(row, rb_magic) = row / group2
+  uint32_t W, W2, S, grid, nq_max;
+  uint32_t rb_magic, rb_one;  // row / group2 = rb_one ? row : umulhi(row, rb_magic)
+  float s_scale;              // 2^-P: keeps (eff - zero2) scale2 2^-P inside fp16
   uint32_t repeat;  // diagnostics: consumers re-run the resident quads this many times
-  uint32_t so_off, part_off, csr_off, x_off, win_off, bar_off;
-  unsigned long long* dbg;  // optional timeline: kTimelineEvents clock64 stamps per CTA
+  uint32_t wait_x;  // x is the previous kernel's output: griddepcontrol.wait before reading it
+  uint32_t pre;     // precompute 1st-order scales of resident units before x
+  uint32_t so_off, part_off, csr_off, x_off, win_off, pre_off, bar_off;
+  unsigned long long* dbg;  // optional timeline: kTimelineEvents stamps per CTA
+  uint32_t dbg_global;      // stamps from %globaltimer (ns) instead of clock64
   uint32_t csr_lo[kMaxGrid + 1];
 };
 
-__device__ __forceinline__ void stamp(unsigned long long* dbg, uint32_t ev) {
-  if (dbg) dbg[blockIdx.x * kTimelineEvents + ev] = clock64();
+__device__ __forceinline__ void stamp_impl(const GemvArgs& a, uint32_t ev) {
+  unsigned long long t;
+  if (a.dbg_global)
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  else
+    t = clock64();
+  a.dbg[blockIdx.x * kTimelineEvents + ev] = t;
 }
+#define stamp(DBG, EV) \
+  do {                 \
+    if (DBG) stamp_impl(a, EV); \
+  } while (0)
 
-// Per-warp reduction window: lane l stores its partial of row r at
-// win[l * kWinStride + r] (16-byte stores, conflict-free); when 32 rows are
-// in, lane r sums row r over the 32 lanes in lane order (deterministic).
-constexpr uint32_t kWinRows = 32, kWinStride = 36;
+// Per-warp reduction window of 16 rows: lane l stores its partial of row r at
+// win[wbase(l) + r], wbase(l) = l * 20 (+16 for l >= 16): 16-byte stores and
+// the transposed reads are both bank-conflict free.  When the window is full,
+// lane l sums row l & 15 over source lanes 16 (l >> 4) .. +15 in lane order,
+// one shuffle joins the halves (fixed order: deterministic).
+constexpr uint32_t kWinRows = 16, kWinWords = 656;
+__device__ __forceinline__ uint32_t win_base(uint32_t l) { return l * 20u + (l >= 16u ? 16u : 0u); }
 
 // KG groups per lane, NQ quads per ring slot (decoded together for ILP),
 // UNI: group2 % 4 == 0 (a quad never straddles 2-order blocks), XSM: x is
-// staged in shared memory before the gather.
+// staged in shared memory (TMA) before the gather.
 template <int KG, int NQ, bool UNI, bool XSM>
 __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
     gemv_kernel(const __grid_constant__ GemvArgs a) {
@@ -196,10 +199,13 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
   float* s_csr = reinterpret_cast<float*>(smem + a.csr_off);
   uint32_t* s_rp = reinterpret_cast<uint32_t*>(s_csr + a.nq_max * 4);
   float* s_prod = reinterpret_cast<float*>(s_rp + a.nq_max * 4 + 4);
+  float* s_red = s_prod + 256;  // [warp] max |x|
   float* s_x = reinterpret_cast<float*>(smem + a.x_off);
+  uint2* s_pre = reinterpret_cast<uint2*>(smem + a.pre_off);
   uint64_t* s_full = reinterpret_cast<uint64_t*>(smem + a.bar_off);
   uint64_t* s_empty = s_full + S;
   uint64_t* s_sobar = s_empty + S;
+  uint64_t* s_xbar = s_sobar + 1;
 
   const uint32_t q0 = (uint32_t)((uint64_t)blockIdx.x * G.quads / a.grid);
   const uint32_t q1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * G.quads / a.grid);
@@ -209,13 +215,14 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
   const uint32_t r_begin = q0 * kRowsPerQuad;
   const uint32_t r_end = min(q1 * kRowsPerQuad, G.rows);
   const uint32_t nrows = r_end - r_begin;
-  const uint32_t rb_first = __umulhi(r_begin, a.rb_magic);
+  auto row_block = [&](uint32_t r) { return a.rb_one ? r : __umulhi(r, a.rb_magic); };
+  const uint32_t rb_first = row_block(r_begin);
 
   if (threadIdx.x < S) {
     mbar_init(&s_full[threadIdx.x], 1);
     mbar_init(&s_empty[threadIdx.x], W);
   }
-  if (threadIdx.x == 32) mbar_init(s_sobar, 1);
+  if (threadIdx.x == 32) mbar_init(s_sobar, 1), mbar_init(s_xbar, 1);
   if (threadIdx.x == 0) stamp(a.dbg, 0);  // entry
   mbar_fence_init();
   __syncthreads();
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
   if (warp == W) {
     // ================= producer: the weight stream does not depend on x
     if (lane == 0) {
-      const uint32_t so_bytes = nrows ? (__umulhi(r_end - 1, a.rb_magic) - rb_first + 1) * G.G2s * 4u : 0u;
+      const uint32_t so_bytes = nrows ? (row_block(r_end - 1) - rb_first + 1) * G.G2s * 4u : 0u;
       if (so_bytes) {
         mbar_expect_tx(s_sobar, so_bytes);
         bulk_load_nohint(smem + a.so_off, a.sorder + (size_t)rb_first * G.G2s, so_bytes, s_sobar);
@@ -232,8 +239,15 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
         mbar_arrive(s_sobar);
       }
       const uint8_t* src = a.quads + (size_t)q0 * dense;
+      const uint32_t npre = min(nunit, S);
       uint32_t slot = 0, phase = 0;
       for (uint32_t u = 0; u < nunit; ++u) {
+        if (u == npre && XSM) {  // resident units queued: now the activation (previous kernel's output)
+          if (a.wait_x) pdl_wait();
+          stamp(a.dbg, 1);  // dependency resolved
+          mbar_expect_tx(s_xbar, G.cols * 4u);
+          bulk_load_nohint(s_x, a.x, G.cols * 4u, s_xbar);
+        }
         const uint32_t bytes = min((uint32_t)NQ, nq - NQ * u) * dense;
         if (u >= S) mbar_wait(&s_empty[slot], phase ^ 1u);
         mbar_expect_tx(&s_full[slot], bytes);
@@ -241,7 +255,12 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
         src += bytes;
         if (++slot == S) slot = 0, phase ^= 1u;
       }
-      stamp(a.dbg, 1);  // all copies issued
+      if (npre == nunit && XSM) {
+        if (a.wait_x) pdl_wait();
+        stamp(a.dbg, 1);  // dependency resolved
+        mbar_expect_tx(s_xbar, G.cols * 4u);
+        bulk_load_nohint(s_x, a.x, G.cols * 4u, s_xbar);
+      }
     }
     return;
   }
@@ -265,7 +284,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
     };
     if (n) fetch(0);
     __syncwarp();
-    if (n) pdl_wait();  // x is the previous kernel's output
+    if (n && a.wait_x) pdl_wait();  // x is the previous kernel's output
     for (uint32_t c0 = 0; c0 < n; c0 += 32u * kPer) {
       const uint32_t c1 = min(c0 + 32u * kPer, n);
 #pragma unroll
@@ -291,12 +310,10 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
   // ================= consumers.  Warps [0, W2) own 2-bit chunks, [W2, W) own
   // 4-bit chunks, so the group type is warp-uniform; lane l of a 2-bit warp
   // owns groups (w + k W2) * 32 + l, of a 4-bit warp blocks (w - W2 + k W4) * 32 + l.
+  // A dead lane (past the last group of its type) decodes a real group with
+  // X = 0, so it contributes exact zeros without a branch in the loop.
   const uint32_t W2 = a.W2, W4 = W - W2;
   const bool two = warp < W2;
-  const uint32_t n2 = G.cols - G.n4;
-  // the lane's groups (index into the row's G groups).  A dead lane (past the
-  // last group of its type) decodes a real group with X = 0 and ex = 0, so it
-  // contributes exact zeros without a branch in the loop.
   uint32_t gk[KG];
   bool lv[KG];
 #pragma unroll
@@ -311,59 +328,15 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
       gk[k] = G.G2 + (lv[k] ? b : G.T4 - 1u);
     }
   }
-  uint32_t pw[KG][8];
-#pragma unroll
-  for (int k = 0; k < KG; ++k) {  // permutation: layer data, before the PDL wait
-    {
-      const uint4* pp = reinterpret_cast<const uint4*>(a.perm + 16u * gk[k]);
-      const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
-      pw[k][0] = p0.x, pw[k][1] = p0.y, pw[k][2] = p0.z, pw[k][3] = p0.w;
-      pw[k][4] = p1.x, pw[k][5] = p1.y, pw[k][6] = p1.z, pw[k][7] = p1.w;
-    }
-  }
-  pdl_wait();  // x is the previous kernel's output
-  if (XSM) {   // stage x with coalesced loads (one L2 sweep per CTA, not 16 gathers per lane)
-    const float4* x4 = reinterpret_cast<const float4*>(a.x);
-    float4* sx4 = reinterpret_cast<float4*>(s_x);
-    const uint32_t n4v = G.cols >> 2;
-    for (uint32_t i = threadIdx.x; i < n4v; i += W * 32) sx4[i] = __ldg(x4 + i);
-    for (uint32_t i = (n4v << 2) + threadIdx.x; i < G.cols; i += W * 32) s_x[i] = __ldg(a.x + i);
-    named_sync(1, W * 32);
-  }
-  half2 X[KG][16];
-  float ex[KG];
-  half2 nsxh[KG];  // zero-point multiplier: z_h * nsxh = z * nsx
-#pragma unroll
-  for (int k = 0; k < KG; ++k) {
-    const uint32_t g = gk[k];
-    const bool live = lv[k];
-    float v[16];
-    const uint32_t s0 = 16u * g;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t c = live ? (pw[k][j >> 1] >> (16 * (j & 1))) & 0xFFFFu : 0u;
-      v[j] = live ? (XSM ? s_x[c] : __ldg(a.x + c)) : 0.0f;
-      if (two && s0 + j >= n2 && s0 + j < G.n2p) v[j] = 0.0f;  // pads (apply_permutation)
-    }
-    const XPrep p = prepare_group(X[k], v, two);
-    ex[k] = live ? p.ex : 0.0f;
-    // 2-bit z lands at 2^(2 sub - 24), 4-bit z at 2^-24
-    const int zp = two ? 2 * (int)(g - 3u * (g / 3u)) : 0;
-    nsxh[k] = __float2half2_rn(live ? p.nsx * pow2f(24 - zp) : 0.0f);
-  }
-  if (threadIdx.x == 0) stamp(a.dbg, 2);  // prologue done
-  mbar_wait(s_sobar, 0);
-
-  if (threadIdx.x == 0 && a.dbg && nunit) {  // diagnostics: when the first unit landed
-    mbar_wait(&s_full[0], 0);
-    stamp(a.dbg, 3);
-  }
-  float* win = reinterpret_cast<float*>(smem + a.win_off) + warp * (32 * kWinStride);
+  float* win = reinterpret_cast<float*>(smem + a.win_off) + warp * kWinWords;
   const uint32_t reps = (a.repeat > 1 && nunit <= S) ? a.repeat : 1;
-  // One consumer loop per group type (warp-uniform), per-lane constants hoisted.
+  const uint32_t npre = a.pre ? min(nunit, S) : 0u;  // units resident before x: scales precomputed
+
+  // One consumer body per group type (warp-uniform), per-lane constants hoisted.
   auto run = [&](auto two_tag) {
     constexpr bool TWO = decltype(two_tag)::value;
     uint32_t off_c[KG], off_p[KG], off_z[KG], zmask[KG], esh[KG], emask[KG];
+    int pe[KG];
 #pragma unroll
     for (int k = 0; k < KG; ++k) {
       const uint32_t g = gk[k];
@@ -374,55 +347,149 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
         off_z[k] = 0;
         zmask[k] = 0x00030003u << (2u * sub);
         // 4/3/3 rule (quantizer.cpp:103-104): eff = scode for sub 0, scode << 1 else;
-        // the masked field reads as eff 2^(pe - 24), pe = 6, 2, 5
+        // the masked field reads as eff 2^(pe - 24)
         esh[k] = sub == 0 ? 0u : 7u;
         emask[k] = sub == 0 ? 0x03C003C0u : (sub == 1 ? 0x00380038u : 0x01C001C0u);
+        pe[k] = sub == 0 ? 6 : (sub == 1 ? 2 : 5);
       } else {
         const uint32_t b = g - G.G2;
         off_c[k] = G.off_c4 + 32u * b;
         off_p[k] = G.off_s4 + 8u * b;
         off_z[k] = G.off_z4 + 2u * b;
         zmask[k] = esh[k] = emask[k] = 0;
+        pe[k] = 0;
       }
     }
-    // 2-order constants per (quad of the unit, k): s = e_f Ae + Bz
+    // ---- 1st-order scales of the lane's 2-bit groups (the 2-order dequant,
+    // engine.cpp:48-63): s1 = (eff - zero2) * scale2, exact in fp32, kept as
+    // fp16 (x 2^-P) for the mixed-precision FMA.  x-independent.
     float Ae[NQ][KG][UNI ? 1 : 4], Bz[NQ][KG][UNI ? 1 : 4];
+    uint32_t rb_end[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) rb_end[j] = 0;
     auto load_scales = [&](int j, uint32_t r0) {
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
-        const int pe = esh[k] == 0 ? 6 : (emask[k] == 0x00380038u ? 2 : 5);
 #pragma unroll
         for (int i = 0; i < (UNI ? 1 : 4); ++i) {
-          const uint32_t rb = __umulhi(min(r0 + i, G.rows - 1), a.rb_magic) - rb_first;
+          const uint32_t rb = row_block(min(r0 + i, G.rows - 1)) - rb_first;
           const uint32_t e = s_so[rb * G.G2s + gk[k]];
-          const float A = half_bits_to_float(e) * ex[k];  // exact: scale2 * 2^k
-          Ae[j][k][i] = A * pow2f(24 - pe);
+          const float A = half_bits_to_float(e) * a.s_scale;  // exact: scale2 * 2^-P
+          Ae[j][k][i] = A * pow2f(24 - pe[k]);
           Bz[j][k][i] = -small_int_to_float(e >> 16) * A;
         }
       }
     };
-    for (uint32_t rep = 0; rep < reps; ++rep) {
-      uint32_t rb_end[NQ];
+    // s1 of rows {0,1} and {2,3} of quad j of the unit in slot base sb, group k
+    auto scales_of = [&](const uint8_t* sb, int j, int k, uint32_t u) -> uint2 {
+      const uint32_t r0 = (q0 + u * NQ + j) * kRowsPerQuad;
+      if (!UNI || r0 >= rb_end[j]) {
+        load_scales(j, r0);
+        rb_end[j] = (row_block(r0) + 1) * G.group2;
+      }
+      const uint2 m = *reinterpret_cast<const uint2*>(sb + j * dense + off_p[k]);
+      const float2 e01 = h2f2((m.x >> esh[k]) & emask[k]);
+      const float2 e23 = h2f2((m.y >> esh[k]) & emask[k]);
+      const float* A = Ae[j][k];
+      const float* B = Bz[j][k];
+      const int i1 = UNI ? 0 : 1, i2 = UNI ? 0 : 2, i3 = UNI ? 0 : 3;
+      return make_uint2(pack_h2(ffma2(e01, make_float2(A[0], A[i1]), make_float2(B[0], B[i1]))),
+                        pack_h2(ffma2(e23, make_float2(A[i2], A[i3]), make_float2(B[i2], B[i3]))));
+    };
+    auto pre_at = [&](uint32_t slot, int j, int k) -> uint2& {
+      return s_pre[((slot * NQ + j) * KG + k) * (W * 32) + warp * 32 + lane];
+    };
+
+    // ---- asynchronous dequantization: while the previous layer still runs
+    // (its output x is not needed yet), decode the 1st-order scales of every
+    // resident unit.
+    if (TWO) {
+      mbar_wait(s_sobar, 0);
+      for (uint32_t u = 0; u < npre; ++u) {
+        mbar_wait(&s_full[u], 0);
+        const uint8_t* sb = smem + (size_t)u * NQ * dense;
 #pragma unroll
-      for (int j = 0; j < NQ; ++j) rb_end[j] = 0;
+        for (int j = 0; j < NQ; ++j)
+#pragma unroll
+          for (int k = 0; k < KG; ++k) pre_at(u, j, k) = scales_of(sb, j, k, u);
+      }
+    }
+
+    // ---- activation prologue: layer-wide power-of-two scale (max|x'| in
+    // [2^10, 2^11): every fp16 x' keeps 11 bits and the group sums of |x'|
+    // stay < 2^15), gather the lane's groups in permuted order.
+    uint32_t pw[KG][8];
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      const uint4* pp = reinterpret_cast<const uint4*>(a.perm + 16u * gk[k]);
+      const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
+      pw[k][0] = p0.x, pw[k][1] = p0.y, pw[k][2] = p0.z, pw[k][3] = p0.w;
+      pw[k][4] = p1.x, pw[k][5] = p1.y, pw[k][6] = p1.z, pw[k][7] = p1.w;
+    }
+    if (threadIdx.x == 0) stamp(a.dbg, 8);  // x-independent work done
+    const float* xs;
+    if (XSM) {
+      mbar_wait(s_xbar, 0);
+      if (threadIdx.x == 0) stamp(a.dbg, 7);  // x landed
+      xs = s_x;
+    } else {
+      if (a.wait_x) pdl_wait();  // x is the previous kernel's output
+      xs = a.x;
+    }
+    float mx = 0.0f;
+    for (uint32_t i = threadIdx.x * 4; i < G.cols; i += W * 128) {
+      const float4 v = XSM ? *reinterpret_cast<const float4*>(xs + i)
+                           : __ldg(reinterpret_cast<const float4*>(xs + i));
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) s_red[warp] = mx;
+    named_sync(1, W * 32);
+    mx = s_red[0];
+    for (uint32_t w2 = 1; w2 < W; ++w2) mx = fmaxf(mx, s_red[w2]);
+    if (threadIdx.x == 0) stamp(a.dbg, 9);  // layer-wide max known
+    const int eb = (int)((__float_as_uint(mx) >> 23) & 0xFFu);
+    const int sh = (eb == 0 ? -126 : eb - 127) - 10;  // floor(log2 max) - 10
+    const uint32_t n2 = G.cols - G.n4;
+    half2 X[KG][16], nsxh[KG];
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      const uint32_t g = gk[k], s0 = 16u * g;
+      float sx = 0.0f;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const uint32_t c = (pw[k][jj >> 1] >> (16 * (jj & 1))) & 0xFFFFu;
+        float v = XSM ? xs[c] : __ldg(xs + c);
+        if (TWO && s0 + jj >= n2 && s0 + jj < G.n2p) v = 0.0f;  // pads (apply_permutation)
+        if (!lv[k]) v = 0.0f;
+        const int b = TWO ? 2 * (jj & 3) : 4 * (jj & 1);
+        const int e = -sh - b;
+        const int e1 = max(-126, min(127, e));
+        const __half h = __float2half_rn(v * pow2f(e1) * pow2f(max(-126, min(127, e - e1))));
+        X[k][jj] = __half2half2(h);
+        sx += __half2float(h) * pow2f(b - 24);
+      }
+      // zero point: z lands at 2^(2 sub - 24) (2-bit) or 2^-24 (4-bit): z_h nsxh = -z sum x'
+      const int zp = TWO ? 2 * (int)(g - 3u * (g / 3u)) : 0;
+      nsxh[k] = __float2half2_rn(-sx * pow2f(24 - zp));
+    }
+    // every accumulated term is in units of 2^(sh + 24) (and 2^P for 2-bit s1)
+    const float yscale = pow2f(max(-126, min(127, sh + 24))) * (TWO ? 1.0f / a.s_scale : 1.0f);
+    if (threadIdx.x == 0) stamp(a.dbg, 2);  // prologue done
+    if (threadIdx.x == 0 && a.dbg && nunit) {  // diagnostics: the first unit is in
+      mbar_wait(&s_full[0], 0);
+      stamp(a.dbg, 3);
+    }
+
+    for (uint32_t rep = 0; rep < reps; ++rep) {
       uint32_t slot = 0, phase = 0, wrow = 0, wrow0 = 0;
       for (uint32_t u = 0; u < nunit; ++u) {
-        const uint32_t qi = u * NQ;
-        if (TWO) {
-#pragma unroll
-          for (int j = 0; j < NQ; ++j) {
-            const uint32_t r0 = (q0 + qi + j) * kRowsPerQuad;
-            if (!UNI || r0 >= rb_end[j]) {
-              load_scales(j, r0);
-              rb_end[j] = (__umulhi(r0, a.rb_magic) + 1) * G.group2;
-            }
-          }
-        }
         mbar_wait(&s_full[slot], phase);
         const uint8_t* sb = smem + (size_t)slot * NQ * dense;
-        float2 acc[NQ][2];
+        float acc[NQ][4];
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) acc[j][0] = acc[j][1] = make_float2(0.0f, 0.0f);
+        for (int j = 0; j < NQ; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0f;
 #pragma unroll
         for (int k = 0; k < KG; ++k) {
           // all NQ quads unconditionally (a short last unit decodes stale slot
@@ -430,27 +497,28 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
           // quads' independent chains interleave
           if (TWO) {
             uint4 w[NQ];
-            uint2 m[NQ];
+            uint2 m[NQ], s1[NQ];
 #pragma unroll
             for (int j = 0; j < NQ; ++j) {
               w[j] = *reinterpret_cast<const uint4*>(sb + j * dense + off_c[k]);
               m[j] = *reinterpret_cast<const uint2*>(sb + j * dense + off_p[k]);
             }
+            if (u < npre) {
+#pragma unroll
+              for (int j = 0; j < NQ; ++j) s1[j] = pre_at(slot, j, k);
+            } else {
+#pragma unroll
+              for (int j = 0; j < NQ; ++j) s1[j] = scales_of(sb, j, k, u);
+            }
 #pragma unroll
             for (int j = 0; j < NQ; ++j) {
-              // ---- 2-bit group: meta, 2-order -> 1-order scale, decode, FMA
-              const half2 D01 = dot2(w[j].x, w[j].y, X[k]);
-              const half2 D23 = dot2(w[j].z, w[j].w, X[k]);
-              const float2 t01 = __half22float2(__hfma2(as_h2(m[j].x & zmask[k]), nsxh[k], D01));
-              const float2 t23 = __half22float2(__hfma2(as_h2(m[j].y & zmask[k]), nsxh[k], D23));
-              const float2 e01 = h2f2((m[j].x >> esh[k]) & emask[k]);
-              const float2 e23 = h2f2((m[j].y >> esh[k]) & emask[k]);
-              const float* A = Ae[j][k];
-              const float* B = Bz[j][k];
-              const int i1 = UNI ? 0 : 1, i2 = UNI ? 0 : 2, i3 = UNI ? 0 : 3;
-              // s1 * ex = (eff - zero2) * scale2 * ex, exact (engine.cpp:48-63)
-              acc[j][0] = ffma2(ffma2(e01, make_float2(A[0], A[i1]), make_float2(B[0], B[i1])), t01, acc[j][0]);
-              acc[j][1] = ffma2(ffma2(e23, make_float2(A[i2], A[i3]), make_float2(B[i2], B[i3])), t23, acc[j][1]);
+              // sum((c - z) x') per row in fp16, then y += s1 * that in fp32
+              const half2 T01 = __hfma2(as_h2(m[j].x & zmask[k]), nsxh[k], dot2(w[j].x, w[j].y, X[k]));
+              const half2 T23 = __hfma2(as_h2(m[j].y & zmask[k]), nsxh[k], dot2(w[j].z, w[j].w, X[k]));
+              acc[j][0] = fhfma_lo(T01, as_h2(s1[j].x), acc[j][0]);
+              acc[j][1] = fhfma_hi(T01, as_h2(s1[j].x), acc[j][1]);
+              acc[j][2] = fhfma_lo(T23, as_h2(s1[j].y), acc[j][2]);
+              acc[j][3] = fhfma_hi(T23, as_h2(s1[j].y), acc[j][3]);
             }
           } else {
             uint4 wa[NQ], wb[NQ];
@@ -464,17 +532,16 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
               s4[j] = *reinterpret_cast<const uint2*>(qb + off_p[k]);
               z4[j] = *reinterpret_cast<const uint16_t*>(qb + off_z[k]);
             }
-            const float2 ex2 = make_float2(ex[k], ex[k]);
 #pragma unroll
             for (int j = 0; j < NQ; ++j) {
-              // ---- 4-bit block
+              // ---- 4-bit block: s4 is fp16 already (fourbit, bitpack.hpp:103-110)
               const uint32_t zz = z4[j] | (z4[j] << 12);
-              const half2 D01 = dot4(wa[j], X[k]);
-              const half2 D23 = dot4(wb[j], X[k]);
-              const float2 t01 = __half22float2(__hfma2(as_h2(zz & 0x000F000Fu), nsxh[k], D01));
-              const float2 t23 = __half22float2(__hfma2(as_h2((zz >> 8) & 0x000F000Fu), nsxh[k], D23));
-              acc[j][0] = ffma2(fmul2(h2f2(s4[j].x), ex2), t01, acc[j][0]);
-              acc[j][1] = ffma2(fmul2(h2f2(s4[j].y), ex2), t23, acc[j][1]);
+              const half2 T01 = __hfma2(as_h2(zz & 0x000F000Fu), nsxh[k], dot4(wa[j], X[k]));
+              const half2 T23 = __hfma2(as_h2((zz >> 8) & 0x000F000Fu), nsxh[k], dot4(wb[j], X[k]));
+              acc[j][0] = fhfma_lo(T01, as_h2(s4[j].x), acc[j][0]);
+              acc[j][1] = fhfma_hi(T01, as_h2(s4[j].x), acc[j][1]);
+              acc[j][2] = fhfma_lo(T23, as_h2(s4[j].y), acc[j][2]);
+              acc[j][3] = fhfma_hi(T23, as_h2(s4[j].y), acc[j][3]);
             }
           }
         }
@@ -484,23 +551,25 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
         }
 #pragma unroll
         for (int j = 0; j < NQ; ++j)
-          *reinterpret_cast<float4*>(win + lane * kWinStride + wrow + 4 * j) =
-              make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
+          *reinterpret_cast<float4*>(win + win_base(lane) + wrow + 4 * j) =
+              make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
         wrow += 4 * NQ;
         if (wrow == kWinRows || u + 1 == nunit) {  // window full: rows over lanes, lane order
           __syncwarp();
-          if (lane < wrow) {
-            float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+          const uint32_t row = lane & 15u, src0 = lane & 16u;
+          float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
 #pragma unroll
-            for (int l = 0; l < 32; l += 4) {
-              s0 += win[(l + 0) * kWinStride + lane];
-              s1 += win[(l + 1) * kWinStride + lane];
-              s2 += win[(l + 2) * kWinStride + lane];
-              s3 += win[(l + 3) * kWinStride + lane];
-            }
-            const uint32_t r = wrow0 + lane;
-            if (r < nrows) s_part[r * W + warp] = (s0 + s1) + (s2 + s3);
+          for (uint32_t l = 0; l < 16; l += 4) {
+            s0 += win[win_base(src0 + l + 0) + row];
+            s1 += win[win_base(src0 + l + 1) + row];
+            s2 += win[win_base(src0 + l + 2) + row];
+            s3 += win[win_base(src0 + l + 3) + row];
           }
+          float sum = (s0 + s1) + (s2 + s3);
+          const float other = __shfl_xor_sync(0xFFFFFFFFu, sum, 16);
+          sum = src0 ? other + sum : sum + other;  // lanes 0-15 first, then 16-31
+          const uint32_t r = wrow0 + row;
+          if (src0 == 0 && row < wrow && r < nrows) s_part[r * W + warp] = sum * yscale;
           __syncwarp();
           wrow0 += wrow, wrow = 0;
         }
@@ -584,7 +653,8 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
   p.uniform_rb = (G.group2 % kRowsPerQuad) == 0;
   p.uq = quads_per_slot(p.kmax, p.uniform_rb);
   p.xsm = G.cols <= 12288;
-  p.rb_magic = (uint32_t)((0x100000000ull + G.group2 - 1) / G.group2);
+  p.rb_one = G.group2 == 1;
+  p.rb_magic = p.rb_one ? 0u : (uint32_t)((0x100000000ull + G.group2 - 1) / G.group2);
   uint32_t so_rows_max = 0;
   for (uint32_t b = 0; b <= p.grid; ++b) {
     const uint32_t q = (uint32_t)((uint64_t)b * G.quads / p.grid);
@@ -597,18 +667,22 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
   }
   const size_t so_bytes = (size_t)so_rows_max * G.G2s * 4;
   const size_t part_bytes = (size_t)p.nq_max * p.warps * 16;
-  const size_t misc_bytes = (size_t)p.nq_max * 4 * 4 + ((size_t)p.nq_max * 4 + 4) * 4 + 256 * 4;
+  const size_t misc_bytes = (size_t)p.nq_max * 4 * 4 + ((size_t)p.nq_max * 4 + 4) * 4 + 256 * 4 + 64 * 4;
   const size_t x_bytes = p.xsm ? align_up((size_t)G.cols * 4, 16) : 0;
-  const size_t win_bytes = (size_t)p.warps * 32 * kWinStride * 4;
+  const size_t win_bytes = (size_t)p.warps * kWinWords * 4;
   const size_t fixed = align_up(so_bytes, 16) + part_bytes + align_up(misc_bytes, 16) + x_bytes +
                        win_bytes + 64;
+  // precomputed 1st-order scales: one uint2 per (slot, quad, k, lane)
+  auto pre_bytes = [&](size_t s) { return s * p.uq * p.kmax * p.warps * 32 * 8; };
   // ring: the CTA's whole quad range when it fits in ~half an SM (so the next
   // layer's CTA fits beside it under PDL), else as many slots as fit
   const size_t unit_bytes = (size_t)p.uq * G.dense_bytes;
   const size_t units = (p.nq_max + p.uq - 1) / p.uq;
   const size_t half_sm = 112 * 1024, full_sm = 220 * 1024;
   size_t S = units;
-  auto total = [&](size_t s) { return align_up(s * unit_bytes, 128) + fixed + (2 * s + 1) * 8; };
+  auto total = [&](size_t s) {
+    return align_up(s * unit_bytes, 128) + fixed + pre_bytes(s) + (2 * s + 2) * 8;
+  };
   while (S > 3 && total(S) > half_sm) --S;
   while (S > 2 && total(S) > full_sm) --S;
   if (total(S) > full_sm) return (int)cudaErrorInvalidConfiguration;
@@ -618,8 +692,9 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
   p.misc_off = p.part_off + (uint32_t)part_bytes;
   p.xg_off = p.misc_off + (uint32_t)align_up(misc_bytes, 16);
   p.win_off = p.xg_off + (uint32_t)x_bytes;
-  p.bar_off = (uint32_t)align_up(p.win_off + win_bytes, 8);
-  p.smem = (uint32_t)(p.bar_off + (2 * S + 1) * 8);
+  p.pre_off = p.win_off + (uint32_t)win_bytes;
+  p.bar_off = (uint32_t)align_up(p.pre_off + pre_bytes(S), 8);
+  p.smem = (uint32_t)(p.bar_off + (2 * S + 2) * 8);
   static bool attr_set = false;  // raise the opt-in limit once per process
   if (!attr_set) {
     for (bool uni : {false, true})
@@ -636,7 +711,8 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
 }
 
 int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream,
-                bool pdl, unsigned long long* dbg, uint32_t repeat) {
+                bool pdl, unsigned long long* dbg, uint32_t repeat, bool global_clock,
+                uint32_t flags) {
   const Geometry& G = L.g;
   const GemvPlan& p = L.plan;
   GemvArgs a;
@@ -647,10 +723,15 @@ int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   a.perm = L.perm16;
   a.g = G;
   a.W = p.warps, a.W2 = p.warps2, a.S = p.nslot;
-  a.grid = p.grid, a.nq_max = p.nq_max, a.rb_magic = p.rb_magic;
-  a.so_off = p.so_off, a.part_off = p.part_off, a.csr_off = p.misc_off, a.x_off = p.xg_off, a.win_off = p.win_off;
+  a.grid = p.grid, a.nq_max = p.nq_max, a.rb_magic = p.rb_magic, a.rb_one = p.rb_one;
+  a.s_scale = p.s_scale;
+  a.so_off = p.so_off, a.part_off = p.part_off, a.csr_off = p.misc_off, a.x_off = p.xg_off, a.win_off = p.win_off, a.pre_off = p.pre_off;
   a.bar_off = p.bar_off;
   a.dbg = dbg;
+  a.dbg_global = global_clock;
+  a.wait_x = (flags & kXIndependent) ? 0u : 1u;
+  a.pre = 1;
+  if (const char* e = std::getenv("QW_NO_PRE")) a.pre = std::atoi(e) ? 0u : 1u;
   a.repeat = repeat;
   std::copy(p.csr_lo, p.csr_lo + p.grid + 1, a.csr_lo);
   const GemvFn fn = pick_kernel(p.kmax, p.uniform_rb, p.xsm);

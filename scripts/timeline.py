@@ -26,7 +26,7 @@ for trial in range(2):
     for _ in range(3):  # warm
         dl.matvec(x, out=y)
     check(lib().qw_debug_timeline(dl._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
-                                  C.c_void_p(st.data_ptr()), REP,
+                                  C.c_void_p(st.data_ptr()), REP, 0,
                                   C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     torch.cuda.synchronize()
     a = st.cpu().numpy().reshape(grid, E).astype(np.int64)
@@ -34,7 +34,7 @@ for trial in range(2):
     print(f"trial {trial}: cycles from entry (mean / max over CTAs)")
     if REP > 1:
         nq = dl.info["quads"] / grid
-        span = d[:, 4] - d[:, 3]
+        span = d[:, 4] - d[:, 2]
         print(f"  repeat {REP}: consumer loop {span.mean():.0f} cycles -> {span.mean() / (REP * nq):.1f} cycles/quad")
     for i in np.argsort(d.mean(0)):
         if d[:, i].max() <= 0 or d[:, i].min() < 0: continue

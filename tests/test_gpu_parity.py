@@ -68,8 +68,15 @@ GEOMS = [
     (40, 512, 0.25, 1, 0.01),      # group2 = 1: every row its own 2-order block
     (21, 768, 0.25, 3, 0.01),      # group2 = 3
     (64, 28672, 0.25, 16, 0.002),  # 70B down width: 56 chunks, 4 per warp
-    (16, 40960, 0.25, 16, 0.002),  # 80 chunks: x reloaded per quad
 ]
+
+
+def test_too_wide_layer_is_rejected_cleanly():
+    """80 chunks of 32 groups exceed the fused kernel's 60: a clean QW_ERR_UNSUPPORTED."""
+    layer = qw.synth_layer(16, 40960, seed=3, alpha=0.25, group2=16, outlier_ratio=0.002)
+    with pytest.raises(qw.QWeightError) as ei:
+        qw.DeviceLayer(layer)
+    assert ei.value.status == 5
 
 
 @pytest.mark.parametrize("rows,cols,alpha,g2,ratio", GEOMS)
