@@ -171,6 +171,15 @@ int qw_matvec(const qw_layer* layer, const float* x, uint32_t batch, float* y,
  * this call starts before the previous kernel on the stream finishes. */
 int qw_matvec_pdl(const qw_layer* layer, const float* x, uint32_t batch,
                   float* y, qw_workspace* ws, void* stream);
+/* Launch flags for qw_matvec_ex. */
+#define QW_LAUNCH_PDL 1u           /* programmatic dependent launch: this call's
+                                      weight stream starts under the previous
+                                      kernel on the stream */
+#define QW_LAUNCH_X_INDEPENDENT 2u /* x was not written by the previous kernel
+                                      on the stream: no dependency wait before
+                                      reading it (q/k/v, gate/up share inputs) */
+int qw_matvec_ex(const qw_layer* layer, const float* x, uint32_t batch, float* y,
+                 qw_workspace* ws, void* stream, uint32_t flags);
 /* Host-buffer, synchronous, checked: length and finiteness as the reference
  * (engine.cpp:124-132).  x_len must equal batch * cols. */
 int qw_matvec_host(const qw_layer* layer, const float* x, uint64_t x_len,
@@ -179,6 +188,8 @@ int qw_matvec_host(const qw_layer* layer, const float* x, uint64_t x_len,
 /* reconstruct_dense (engine.hpp:26): w device fp32 [rows][padded_cols],
  * permuted order, bit-exact with the reference. */
 int qw_dequant(const qw_layer* layer, float* w, void* stream);
+/* Same with a host buffer of rows * padded_cols floats, synchronous. */
+int qw_dequant_host(const qw_layer* layer, float* w, uint64_t w_len);
 /* unpack_layer (bitpack.hpp:128): device u8 outputs
  * codes2 [rows][n2_padded], zeros2 [rows][groups_per_row],
  * scodes [rows][groups_per_row], codes4 [rows][n4]. */

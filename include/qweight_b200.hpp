@@ -1,0 +1,131 @@
+// qweight_b200.hpp -- C++ drop-in for the reference's hot-path API.
+//
+// The reference (arXiv 2311.16442 artifact, namespace qweight) exposes its
+// hot path as C++ functions over a PackedLayer (proj/include/qweight/
+// engine.hpp:26-36):
+//
+//   WeightMatrix reconstruct_dense(const PackedLayer&);
+//   MatvecResult matvec_oracle(const PackedLayer&, std::span<const float> x);
+//   MatvecResult matvec_pipelined(const PackedLayer&, std::span<const float>, unsigned workers);
+//
+// This header adds the B200 path under qweight::b200 with the same parameter
+// and return types, without touching the reference headers.  It is header
+// only and needs nothing but the reference's include/ directory and
+// libqweight_b200.so (the extern "C" layer in qweight_b200.h): status codes
+// are turned back into qweight::Error (types.hpp:11-14), the layer is
+// uploaded once into an owning DeviceLayer (validate_layer + device repack),
+// and every call is checked like the reference (length and finiteness of x,
+// engine.cpp:124-132; workers == 0 rejected, engine.cpp:187-188).
+//
+// Numerics: reconstruct_dense is bit-identical to the reference; y matches
+// matvec_reference_f64 within 1e-2 relative (typically ~1e-3; fp16 partial
+// sums inside each 16-channel group, fp32 across groups) -- it is NOT the
+// reference's bitwise sequential-fp32 order, so keep the reference's
+// matvec_pipelined for the bitwise acceptance criterion (SPEC.md AC5).
+#pragma once
+
+#include <chrono>
+#include <cstdint>
+#include <span>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "qweight/bitpack.hpp"
+#include "qweight/engine.hpp"
+#include "qweight/types.hpp"
+#include "qweight_b200.h"
+
+namespace qweight::b200 {
+
+inline void check(int status) {
+  if (status != QW_OK)
+    throw qweight::Error(std::string(qw_strerror(status)) + ": " + qw_last_error());
+}
+
+// A PackedLayer resident in B200 HBM (device repack of bitpack.hpp:15-22).
+class DeviceLayer {
+ public:
+  explicit DeviceLayer(const PackedLayer& L, int device = 0) : rows_(L.cfg.rows), cols_(L.cfg.cols) {
+    // sorder / fourbit are padded structs (sizeof 4): pass structure-of-arrays
+    std::vector<uint8_t> z2(L.sorder.size()), z4(L.fourbit.size());
+    std::vector<uint16_t> s2(L.sorder.size()), s4(L.fourbit.size());
+    for (size_t i = 0; i < L.sorder.size(); ++i) z2[i] = L.sorder[i].zero2, s2[i] = L.sorder[i].scale2;
+    for (size_t i = 0; i < L.fourbit.size(); ++i) z4[i] = L.fourbit[i].zero, s4[i] = L.fourbit[i].scale;
+    qw_layer_view v{};
+    v.n = L.cfg.n, v.n2 = L.cfg.n2, v.group1 = L.cfg.group1, v.group2 = L.cfg.group2;
+    v.tile = L.cfg.tile, v.rows = L.cfg.rows, v.cols = L.cfg.cols, v.n4 = L.cfg.n4;
+    v.pad2 = L.cfg.pad2, v.outlier_count = L.cfg.outlier_count;
+    v.alpha = L.cfg.alpha, v.outlier_ratio = L.cfg.outlier_ratio;
+    v.plan_bits = L.plan.bits.data(), v.plan_bits_len = L.plan.bits.size();
+    v.plan_perm = L.plan.perm.data(), v.plan_perm_len = L.plan.perm.size();
+    v.main = L.main.data(), v.main_len = L.main.size();
+    v.tail2 = L.tail2.data(), v.tail2_len = L.tail2.size();
+    v.tail4 = L.tail4.data(), v.tail4_len = L.tail4.size();
+    v.secondary = L.secondary.data(), v.secondary_len = L.secondary.size();
+    v.meta = L.meta.data(), v.meta_len = L.meta.size();
+    v.sorder_zero2 = z2.data(), v.sorder_scale2 = s2.data(), v.sorder_len = z2.size();
+    v.fourbit_scale = s4.data(), v.fourbit_zero = z4.data(), v.fourbit_len = z4.size();
+    v.csr_row_ptr = L.csr.row_ptr.data(), v.csr_row_ptr_len = L.csr.row_ptr.size();
+    v.csr_col_ind = L.csr.col_ind.data(), v.csr_values = L.csr.values.data();
+    v.csr_nnz = L.csr.col_ind.size();
+    check(qw_layer_upload(&v, device, &layer_));
+    check(qw_workspace_create(device, L.plan.padded_channels(), 16, &ws_));
+    qw_layer_info info{};
+    check(qw_layer_get_info(layer_, &info));
+    padded_cols_ = info.padded_cols;
+  }
+  DeviceLayer(const DeviceLayer&) = delete;
+  DeviceLayer& operator=(const DeviceLayer&) = delete;
+  ~DeviceLayer() {
+    if (ws_) qw_workspace_free(ws_);
+    if (layer_) qw_layer_free(layer_);
+  }
+  uint32_t rows() const { return rows_; }
+  uint32_t cols() const { return cols_; }
+  uint32_t padded_cols() const { return padded_cols_; }
+
+  // matvec_oracle / matvec_pipelined shape: host x in, MatvecResult out.
+  // stage_ns stays zero (one fused kernel has no CPU stage split); wall_ns
+  // is the host wall clock of the checked call, copies included.
+  MatvecResult matvec(std::span<const float> x) const {
+    MatvecResult r;
+    r.y.assign(rows_, 0.0f);
+    const auto t0 = std::chrono::steady_clock::now();
+    check(qw_matvec_host(layer_, x.data(), x.size(), 1, r.y.data(), ws_, nullptr));
+    r.wall_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                    std::chrono::steady_clock::now() - t0).count();
+    return r;
+  }
+  // reconstruct_dense: rows x padded_cols, permuted order, bit-exact
+  WeightMatrix reconstruct_dense() const {
+    WeightMatrix w;
+    w.rows = rows_, w.cols = padded_cols_;
+    w.data.assign((size_t)rows_ * padded_cols_, 0.0f);
+    check(qw_dequant_host(layer_, w.data.data(), w.data.size()));
+    return w;
+  }
+  const qw_layer* handle() const { return layer_; }
+
+ private:
+  qw_layer* layer_ = nullptr;
+  qw_workspace* ws_ = nullptr;
+  uint32_t rows_ = 0, cols_ = 0, padded_cols_ = 0;
+};
+
+// Free functions with the reference's exact signatures (engine.hpp:26-36).
+// Each call uploads the layer (validate_layer included); hold a DeviceLayer
+// to amortise the upload over many calls.
+inline WeightMatrix reconstruct_dense(const PackedLayer& layer) {
+  return DeviceLayer(layer).reconstruct_dense();
+}
+inline MatvecResult matvec_oracle(const PackedLayer& layer, std::span<const float> x) {
+  return DeviceLayer(layer).matvec(x);
+}
+inline MatvecResult matvec_pipelined(const PackedLayer& layer, std::span<const float> x,
+                                     unsigned workers) {
+  if (workers == 0) throw qweight::Error("matvec_pipelined: workers must be >= 1");
+  return DeviceLayer(layer).matvec(x);
+}
+
+}  // namespace qweight::b200

@@ -85,6 +85,9 @@ _SIGS = {
     "qw_workspace_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
     "qw_workspace_free": (C.c_int, [C.c_void_p]),
     "qw_matvec": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "qw_matvec_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_uint32]),
+    "qw_dequant_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "qw_matvec_pdl": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
                                 C.c_void_p]),
     "qw_matvec_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
@@ -100,6 +103,10 @@ _SIGS = {
 }
 
 _lib = None
+
+
+def lib_path() -> Path:
+    return LIB_PATH
 
 
 def lib() -> C.CDLL:

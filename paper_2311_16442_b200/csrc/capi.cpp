@@ -287,7 +287,7 @@ int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
 }
 
 int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_workspace* ws,
-               void* stream, bool pdl) {
+               void* stream, bool pdl, uint32_t flags = 0) {
   if (int s = check_ws(L, ws, batch)) return s;
   if (!x || !y) return fail(QW_ERR_ARG, "matvec: null activation or output");
   int dev_now = -1;
@@ -296,7 +296,8 @@ int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_w
     cudaError_t e = cudaSetDevice(L->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   }
-  const int e = qwdev::launch_gemv(L->dev, x, batch, y, stream, pdl);
+  const int e = qwdev::launch_gemv(L->dev, x, batch, y, stream, pdl, nullptr, 1, false,
+                                   (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u);
   if (e) return cuda_fail((cudaError_t)e, "gemv launch");
   return QW_OK;
 }
@@ -573,6 +574,11 @@ int qw_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_wo
   return run_matvec(L, x, batch, y, ws, stream, false);
 }
 
+int qw_matvec_ex(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_workspace* ws,
+                 void* stream, uint32_t flags) {
+  return run_matvec(L, x, batch, y, ws, stream, (flags & QW_LAUNCH_PDL) != 0, flags);
+}
+
 int qw_matvec_pdl(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_workspace* ws,
                   void* stream) {
   return run_matvec(L, x, batch, y, ws, stream, true);
@@ -614,6 +620,22 @@ int qw_dequant(const qw_layer* L, float* w, void* stream) {
   cudaSetDevice(L->device);
   const int e = qwdev::launch_dequant(L->dev, w, stream);
   return e ? cuda_fail((cudaError_t)e, "dequant launch") : QW_OK;
+}
+
+int qw_dequant_host(const qw_layer* L, float* w, uint64_t w_len) {
+  if (!L || !w) return fail(QW_ERR_ARG, "dequant: null argument");
+  const uint64_t n = (uint64_t)L->info.rows * L->info.padded_cols;
+  if (w_len != n) return fail(QW_ERR_ARG, "dequant: output length != rows * padded_cols");
+  cudaSetDevice(L->device);
+  float* dw = nullptr;
+  cudaError_t e = cudaMalloc((void**)&dw, n * 4 + 4);
+  if (e != cudaSuccess) return cuda_fail(e, "alloc w");
+  int status = QW_OK;
+  if (int k = qwdev::launch_dequant(L->dev, dw, nullptr)) status = cuda_fail((cudaError_t)k, "dequant launch");
+  if (!status && (e = cudaMemcpy(w, dw, n * 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    status = cuda_fail(e, "copy w");
+  cudaFree(dw);
+  return status;
 }
 
 int qw_unpack(const qw_layer* L, uint8_t* codes2, uint8_t* zeros2, uint8_t* scodes, uint8_t* codes4,

@@ -595,10 +595,16 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
 
 using GemvFn = void (*)(GemvArgs);
 
+uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? (uint32_t)std::atoi(e) : dflt;
+}
 template <bool UNI, bool XSM>
 GemvFn pick2(uint32_t kg) {
   switch (kg) {
-    case 1: return gemv_kernel<1, UNI ? 4 : 1, UNI, XSM>;
+    case 1:
+      if (UNI && env_u32("QW_NQ1", 2) == 2) return gemv_kernel<1, 2, UNI, XSM>;
+      return gemv_kernel<1, UNI ? 4 : 1, UNI, XSM>;
     case 2: return gemv_kernel<2, UNI ? 2 : 1, UNI, XSM>;
     case 3: return gemv_kernel<3, 1, UNI, XSM>;
     default: return gemv_kernel<4, 1, UNI, XSM>;
@@ -608,7 +614,9 @@ GemvFn pick_kernel(uint32_t kg, bool uni, bool xsm) {
   return uni ? (xsm ? pick2<true, true>(kg) : pick2<true, false>(kg))
              : (xsm ? pick2<false, true>(kg) : pick2<false, false>(kg));
 }
-uint32_t quads_per_slot(uint32_t kg, bool uni) { return !uni ? 1u : (kg == 1 ? 4u : (kg == 2 ? 2u : 1u)); }
+uint32_t quads_per_slot(uint32_t kg, bool uni) {
+  return !uni ? 1u : (kg == 1 ? env_u32("QW_NQ1", 2) : (kg == 2 ? 2u : 1u));
+}
 
 cudaError_t launch_ex(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                       bool pdl, void** params) {
@@ -678,7 +686,7 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
   // layer's CTA fits beside it under PDL), else as many slots as fit
   const size_t unit_bytes = (size_t)p.uq * G.dense_bytes;
   const size_t units = (p.nq_max + p.uq - 1) / p.uq;
-  const size_t half_sm = 112 * 1024, full_sm = 220 * 1024;
+  const size_t half_sm = env_u32("QW_SMEM_KB", 112) * 1024, full_sm = 220 * 1024;
   size_t S = units;
   auto total = [&](size_t s) {
     return align_up(s * unit_bytes, 128) + fixed + pre_bytes(s) + (2 * s + 2) * 8;
@@ -705,6 +713,11 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
                                                  (int)(227 * 1024));
           if (err != cudaSuccess) return (int)err;
         }
+    for (bool xsm : {false, true}) {
+      cudaError_t err = cudaFuncSetAttribute(xsm ? gemv_kernel<1, 2, true, true> : gemv_kernel<1, 2, true, false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+      if (err != cudaSuccess) return (int)err;
+    }
     attr_set = true;
   }
   return 0;

@@ -113,9 +113,12 @@ class DeviceLayer:
 
     # ---------------------------------------------------------------- forward
     def matvec(self, x, out=None, workspace: Workspace | None = None, stream=None,
-               pdl: bool = False):
+               pdl: bool = False, x_independent: bool = False):
         """y = W_q x on the GPU.  x: torch cuda fp32 [cols] or [batch, cols]
-        in original channel order.  Returns fp32 [rows] / [batch, rows]."""
+        in original channel order.  Returns fp32 [rows] / [batch, rows].
+        pdl: programmatic dependent launch (weights stream under the previous
+        kernel); x_independent: x was not produced by the previous kernel on
+        the stream, so no dependency wait is needed before reading it."""
         if torch is None:
             raise QWeightError(3, "torch is required for device tensors")
         squeeze = x.dim() == 1
@@ -128,9 +131,10 @@ class DeviceLayer:
         if out is None:
             out = torch.empty((batch, self.rows), dtype=torch.float32, device=xb.device)
         ws = workspace or default_workspace(self.device)
-        fn = lib().qw_matvec_pdl if pdl else lib().qw_matvec
-        check(fn(self._h, C.c_void_p(xb.data_ptr()), batch, C.c_void_p(out.data_ptr()), ws._h,
-                 C.c_void_p(_stream_handle(stream))))
+        flags = (1 if pdl else 0) | (2 if x_independent else 0)
+        check(lib().qw_matvec_ex(self._h, C.c_void_p(xb.data_ptr()), batch,
+                                 C.c_void_p(out.data_ptr()), ws._h,
+                                 C.c_void_p(_stream_handle(stream)), flags))
         return out.reshape(-1) if squeeze else out
 
     def matvec_checked(self, x: np.ndarray, workspace: Workspace | None = None) -> MatvecResult:

@@ -30,8 +30,12 @@ class _Slot:
 
 class LinearStack:
     def __init__(self, layers: list[DeviceLayer], device: int = 0, batch: int = 1,
-                 pdl: bool = True):
+                 pdl: bool = True, depends: list[bool] | None = None):
+        """depends[i]: linear i reads an input produced by linear i-1 (it
+        waits for it); False lets it read its input at once (its input came
+        from the host or an earlier, finished kernel)."""
         self.device, self.batch, self.pdl = device, batch, pdl
+        self.depends = list(depends) if depends is not None else [True] * len(layers)
         self.dev = torch.device(f"cuda:{device}")
         xo = yo = 0
         self.slots = []
@@ -61,14 +65,14 @@ class LinearStack:
     def launch_step(self, stream=None):
         for i, s in enumerate(self.slots):
             s.layer.matvec(self.x_of(i), out=self.y_of(i), workspace=self.ws, stream=stream,
-                           pdl=self.pdl)
+                           pdl=self.pdl, x_independent=not self.depends[i])
 
     def launch_subset(self, select, stream=None):
         """Launch only the linears `select(layer)` accepts (kernel-only timing)."""
         for i, s in enumerate(self.slots):
             if select(s.layer):
                 s.layer.matvec(self.x_of(i), out=self.y_of(i), workspace=self.ws, stream=stream,
-                               pdl=self.pdl)
+                               pdl=self.pdl, x_independent=not self.depends[i])
 
     def capture(self):
         """Capture one decode step into a CUDA graph (after a warm run)."""

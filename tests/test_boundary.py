@@ -1,0 +1,84 @@
+"""The drop-in boundary, checked without a GPU.
+
+  * libqweight_b200.so exports every entry point include/qweight_b200.h
+    declares (the C-ABI a reference-side binding links against);
+  * the C++ shim include/qweight_b200.hpp compiles and links against the
+    reference's own headers (proj/include/qweight/*.hpp), i.e. the
+    reference's API types go straight in (skipped where /root/reference is
+    absent, e.g. on the GPU box);
+  * status codes and messages behave like qweight::Error on bad input.
+"""
+import re
+import shutil
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2311_16442_b200 as qw
+from paper_2311_16442_b200 import _native
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "qweight_b200.h"
+REF_INC = Path("/root/reference/proj/include")
+
+
+def declared_functions() -> set[str]:
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return set(re.findall(r"\b(qw_[a-z0-9_]+)\s*\(", text))
+
+
+def exported_dynamic() -> set[str]:
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_native.lib_path())],
+                         capture_output=True, text=True, check=True).stdout
+    return {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+
+
+def test_every_declared_entry_point_is_exported():
+    declared = declared_functions()
+    assert len(declared) >= 30
+    missing = declared - exported_dynamic()
+    assert not missing, missing
+
+
+def test_python_binding_covers_the_header():
+    assert declared_functions() <= set(qw.exported_symbols())
+
+
+def test_abi_version_and_strerror():
+    L = qw.lib()
+    assert L.qw_abi_version() == 1
+    assert L.qw_strerror(0) == b"ok"
+    assert L.qw_strerror(2) == b"invalid layer"
+    assert L.qw_strerror(99) == b"unknown status"
+
+
+def test_invalid_view_is_rejected_with_layer_status():
+    import dataclasses
+    layer = qw.synth_layer(8, 64, seed=1)
+    bad = dataclasses.replace(layer, meta=layer.meta[:-1])
+    with pytest.raises(qw.QWeightError) as ei:
+        qw.validate_layer(bad)
+    assert ei.value.status == 2
+
+
+@pytest.mark.skipif(not REF_INC.exists() or shutil.which("g++") is None,
+                    reason="reference headers not present (GPU box)")
+def test_cpp_shim_compiles_against_reference_headers(tmp_path):
+    src = tmp_path / "shim.cpp"
+    src.write_text(
+        '#include "qweight_b200.hpp"\n'
+        "int main() {\n"
+        "  qweight::PackedLayer L;\n"
+        "  try { qweight::b200::matvec_pipelined(L, std::span<const float>{}, 0); }\n"
+        "  catch (const qweight::Error&) { return qw_abi_version() == 1 ? 0 : 2; }\n"
+        "  return 1;\n"
+        "}\n")
+    exe = tmp_path / "shim"
+    lib_dir = _native.lib_path().parent
+    subprocess.run(["g++", "-std=c++20", f"-I{REF_INC}", f"-I{ROOT / 'include'}", str(src),
+                    f"-L{lib_dir}", "-lqweight_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)],
+                   check=True)
+    # workers == 0 throws qweight::Error before touching the device (engine.cpp:187-188)
+    assert subprocess.run([str(exe)]).returncode == 0
