@@ -212,6 +212,11 @@ int qw_debug_timeline(const qw_layer* layer, const float* x, float* y,
                       unsigned long long* stamps, uint32_t repeat, uint32_t flags,
                       void* stream);
 int qw_debug_timeline_events(void);
+/* Diagnostics: one batched (K4) matvec stamping %globaltimer per CTA into
+ * stamps [grid][8]: 0 setup, 1 first A tile, 2 last A tile, 3 accumulator
+ * ready, 4 epilogue staged, 5 split partials parked, 6 y stored. */
+int qw_debug_gemm_timeline(const qw_layer* layer, const float* x, uint32_t batch, float* y,
+                           unsigned long long* stamps, void* stream);
 
 /* Number of kernels one qw_matvec call launches. */
 int qw_launches_per_matvec(const qw_layer* layer, uint32_t batch);

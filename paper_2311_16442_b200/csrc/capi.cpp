@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <memory>
@@ -41,6 +42,7 @@ struct qw_layer {
   qwdev::DeviceLayer dev;
   int device = 0;
   int num_sms = 148;
+  float max_scale2 = 0.0f, max_s4 = 0.0f;  // for the batched path's fp16 range
   qw_layer_info info{};
 };
 
@@ -271,6 +273,7 @@ cudaError_t upload(T** dst, const std::vector<T>& src, size_t min_elems = 1) {
 }
 
 void free_dev(qwdev::DeviceLayer& d) {
+  qwdev::free_gemm(d);
   cudaFree(d.quads), cudaFree(d.sorder), cudaFree(d.perm), cudaFree(d.row_ptr), cudaFree(d.csr);
   cudaFree(d.perm16);
   d = qwdev::DeviceLayer{};
@@ -296,8 +299,11 @@ int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_w
     cudaError_t e = cudaSetDevice(L->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   }
-  const int e = qwdev::launch_gemv(L->dev, x, batch, y, stream, pdl, nullptr, 1, false,
-                                   (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u);
+  static const bool no_gemm = std::getenv("QW_NO_GEMM") != nullptr;
+  const int e = (batch >= 2 && L->dev.gemm.ok && !no_gemm)
+                    ? qwdev::launch_gemm(L->dev, x, batch, y, stream)
+                    : qwdev::launch_gemv(L->dev, x, batch, y, stream, pdl, nullptr, 1, false,
+                                         (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u);
   if (e) return cuda_fail((cudaError_t)e, "gemv launch");
   return QW_OK;
 }
@@ -514,6 +520,10 @@ int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
       int P = 0;
       if (mx > 0.0f && std::isfinite(mx)) P = std::ilogb(15.0f * mx) - 14;
       H->dev.plan.s_scale = std::ldexp(1.0f, -std::max(-100, std::min(100, P)));
+      H->max_scale2 = mx;
+      float m4 = 0.0f;
+      for (const auto& fb : L.fourbit) m4 = std::max(m4, std::fabs(qwb::f16_to_f32(fb.scale)));
+      H->max_s4 = m4;
     }
     if ((e = upload(&H->dev.quads, quads)) != cudaSuccess ||
         (e = upload(&H->dev.sorder, sorder)) != cudaSuccess ||
@@ -523,6 +533,10 @@ int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
         (e = upload(&H->dev.perm16, perm16)) != cudaSuccess) {
       free_dev(H->dev);
       return cuda_fail(e, "upload");
+    }
+    if (int ge = qwdev::plan_gemm(H->dev, H->num_sms, H->max_scale2, H->max_s4)) {
+      free_dev(H->dev);
+      return cuda_fail((cudaError_t)ge, "gemm plan");
     }
     *out = H.release();
     return (int)QW_OK;
@@ -670,6 +684,12 @@ int qw_layer_clone(const qw_layer* L, qw_layer** out) {
     free_dev(H->dev);
     return cuda_fail(e, "clone");
   }
+  H->max_scale2 = L->max_scale2, H->max_s4 = L->max_s4;
+  H->dev.gemm = qwdev::GemmPlan{};
+  if (int ge = qwdev::plan_gemm(H->dev, H->num_sms, H->max_scale2, H->max_s4)) {
+    free_dev(H->dev);
+    return cuda_fail((cudaError_t)ge, "gemm plan");
+  }
   *out = H.release();
   return QW_OK;
 }
@@ -683,10 +703,19 @@ int qw_debug_timeline(const qw_layer* L, const float* x, float* y, unsigned long
   return e ? cuda_fail((cudaError_t)e, "gemv launch") : QW_OK;
 }
 
+int qw_debug_gemm_timeline(const qw_layer* L, const float* x, uint32_t batch, float* y,
+                           unsigned long long* stamps, void* stream) {
+  if (!L || !x || !y || !stamps) return fail(QW_ERR_ARG, "timeline: null argument");
+  if (!L->dev.gemm.ok || batch < 2 || batch > 16) return fail(QW_ERR_UNSUPPORTED, "timeline: no batched path");
+  cudaSetDevice(L->device);
+  const int e = qwdev::launch_gemm(L->dev, x, batch, y, stream, stamps);
+  return e ? cuda_fail((cudaError_t)e, "gemm launch") : QW_OK;
+}
+
 int qw_debug_timeline_events(void) { return (int)qwdev::kTimelineEvents; }
 
 int qw_launches_per_matvec(const qw_layer* L, uint32_t batch) {
-  (void)L;
+  if (L && batch >= 2 && L->dev.gemm.ok && !std::getenv("QW_NO_GEMM")) return 2;  // x prologue (+ CSR), GEMM
   return (int)batch;
 }
 

@@ -52,9 +52,27 @@ struct GemvPlan {
   uint32_t csr_lo[kMaxGrid + 1] = {};  // first CSR entry of each CTA's rows
 };
 
+// Batched (2..16 columns) tensor-core plan: 128-row M tiles x KS K splits of
+// 2-tile stages (96 2-bit + 32 4-bit channels); TMA 2-D boxes of the quad
+// records; 1st-order scales applied while dequantizing into the A tile.
+struct GemmPlan {
+  uint32_t ok = 0;           // layer geometry supported (paired tiles, group2 % 4 == 0)
+  uint32_t tiles = 0, ks = 1, stages = 0, wstages = 0;  // M tiles, K splits, 2-tile sub-stages and 8-tile weight stages per row
+  int shift = 0;             // A tile holds w * 2^-shift (keeps fp16 scales in range)
+  alignas(64) uint8_t tmap[5][128];  // CUtensorMap: code2, meta, code4, s4, z4 boxes
+  alignas(64) uint8_t tmap_so[128];  // CUtensorMap: sorder box of a tile's row blocks
+  uint32_t so_rows = 0;
+  float* partial = nullptr;  // [ks][16][rows] split-K partial sums
+  uint32_t* counters = nullptr;  // [tiles] split-K arrivals (self-resetting)
+  uint16_t* xpt = nullptr;   // [stages][128 k][16 n] fp16 B tiles (UMMA K-major layout)
+  int* xexp = nullptr;       // [16] per-column power-of-two exponents
+  float* ycsr = nullptr;     // [16][rows] CSR outlier sums of the call
+};
+
 struct DeviceLayer {
   Geometry g;
   GemvPlan plan;
+  GemmPlan gemm;
   uint8_t* quads = nullptr;      // quads * dense_bytes
   uint32_t* sorder = nullptr;    // row_blocks * G2s
   uint32_t* perm = nullptr;      // padded_cols (0xFFFFFFFF = pad)
@@ -83,6 +101,12 @@ int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
                 bool pdl, unsigned long long* dbg = nullptr, uint32_t repeat = 1,
                 bool global_clock = false, uint32_t flags = 0);
 int launch_dequant(const DeviceLayer& L, float* w, void* stream);
+// Batched path (K4): plan at upload (allocates the layer's split-K scratch),
+// launch = x prologue + tcgen05 GEMM.  free_gemm releases the scratch.
+int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4);
+void free_gemm(DeviceLayer& L);
+int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream,
+                unsigned long long* dbg = nullptr);  // 3 launches: x prologue, CSR, GEMM
 int launch_unpack(const DeviceLayer& L, uint8_t* codes2, uint8_t* zeros2, uint8_t* scodes,
                   uint8_t* codes4, void* stream);
 

@@ -1,0 +1,578 @@
+// qw_gemm.cu -- K4: the batched (2..16 activation columns) quantized linear on
+// the 5th-generation tensor cores (north-star (d)).
+//
+// Same semantics as K2 (matvec_oracle per column, engine.cpp:169-183), but
+// here the layer is a dense contraction, so the weights are dequantized once
+// into fp16 tiles in shared memory and fed to tcgen05.mma (kind::f16, M=128,
+// N=16, fp32 accumulation in TMEM) against the 16 activation columns.
+//
+//   xprep_kernel  one CTA per column n: x_n gathered into permuted order
+//                 (apply_permutation, plan.cpp:107-116; pads 0), scaled by a
+//                 power of two 2^-e_n (max |x'| in [2^14, 2^15)), stored as
+//                 fp16 B tiles already in the UMMA K-major core-matrix layout
+//                 (one contiguous 4 KB block per 128-channel stage).
+//   gemm_kernel   CTA = (128-row M tile, K split).  Warp 0: TMA 2-D boxes of
+//                 the quad records (code2 / meta / code4 / s4 / z4 of 32 quads
+//                 per stage) + the stage's B tile.  Warps 2-9: dequantize one
+//                 (quad, group) item each per stage -- the 2-order dequant
+//                 s1 = (eff - zero2) * scale2 (engine.cpp:48-63) folded into
+//                 w = (c - z) s1 with exactly one rounding to fp16 -- into an
+//                 MN-major A tile (row pairs are adjacent M elements, so the
+//                 packed fp16x2 results store directly; SBO/LBO chosen so the
+//                 8-byte stores are bank-conflict free).  Warp 1: one thread
+//                 issues 8 tcgen05.mma per stage, tcgen05.commit frees the A/B
+//                 buffers.  Warps 2-5 read the 128x16 accumulator with
+//                 tcgen05.ld, undo the power-of-two scales, add the CSR
+//                 outliers (exact fp32) and store y -- or, with K splits, park
+//                 partials; the last CTA of a tile sums them in split order
+//                 (deterministic).
+//
+// A tile value = RN_fp16((c - z) * (eff - zero2) * scale2 * 2^-P): the
+// integer part is formed exactly by one HFMA2 on subnormal-coded operands
+// (c 2^(b-24) * m 2^(12-b) + (-z m 2^-12)), the scale by one HMUL2, so each
+// tile element is the correctly rounded fp16 of the reference's fp32 weight
+// (reconstruct_dense) times 2^-P.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "qw_device.hpp"
+#include "qw_ptx.cuh"
+
+namespace qwdev {
+namespace {
+
+constexpr uint32_t kTileRows = 128, kTileQuads = 32;
+constexpr uint32_t kStageK = 128;              // MMA sub-stage: 2 tiles = 96 2-bit + 32 4-bit channels
+constexpr uint32_t kSubPerW = 4;               // a weight stage holds 4 sub-stages (8 tiles)
+constexpr uint32_t kASbo = 144, kALbo = 2320;  // A tile: m-block / k-block strides (bytes)
+constexpr uint32_t kATileBytes = 16 * kALbo;   // 16 k-blocks
+constexpr uint32_t kBStageBytes = kStageK * 16 * 2;  // 4 KB: 8 slabs of 16 k x 16 n
+// weight stage in shared memory: [32 quads][box] per field, boxes in u32 units
+// over 8 tiles (wide rows keep the TMA request count low), plus the 2-order
+// params of the tile's row blocks [<= 33][24 groups] (read from shared memory:
+// a global load in flight would stall the async-proxy fence that publishes A)
+constexpr uint32_t kBoxC2 = 96, kBoxMeta = 16, kBoxC4 = 64, kBoxS4 = 16, kBoxZ4 = 4;  // u32
+constexpr uint32_t kSoBoxG = 24, kSoRowsMax = 33;
+constexpr uint32_t kOffC2 = 0, kOffMeta = kOffC2 + 32 * kBoxC2 * 4, kOffC4 = kOffMeta + 32 * kBoxMeta * 4,
+                   kOffS4 = kOffC4 + 32 * kBoxC4 * 4, kOffZ4 = kOffS4 + 32 * kBoxS4 * 4,
+                   kOffSo = kOffZ4 + 32 * kBoxZ4 * 4,
+                   kWStageBytes = (kOffSo + kSoRowsMax * kSoBoxG * 4 + 1023) / 1024 * 1024;  // 28 KB
+constexpr uint32_t kWSlots = 2, kBSlots = 8, kABufs = 3;
+constexpr uint32_t kDqWarps = 16;
+constexpr uint32_t kThreads = (2 + kDqWarps) * 32;
+
+// ---------------------------------------------------------------- PTX
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_addr(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);  // no swizzle, sm100 version
+}
+// kind::f16, D f32, A f16 MN-major, B f16 K-major, N = 16, M = 128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 15) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t h2u(half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ float p2(int e) { return __uint_as_float((uint32_t)(max(-126, min(127, e)) + 127) << 23); }
+
+// ---------------------------------------------------------------- x prologue
+// Column n of x (original order) -> fp16 B tiles in stage order: stage st
+// holds 2-bit permuted channels [96 st, 96 st + 96) then 4-bit channels
+// n2p + [32 st, 32 st + 32); element (k, n) of a stage at
+// (k % 8) * 2 + (n % 8) * 16 + (n / 8) * 128 + (k / 8) * 256.
+// Grid (chunks, 16): every CTA re-derives its column's power-of-two scale
+// from a full (L2-resident, independent-load) max, then converts one
+// element per thread, so no thread waits on a chain of dependent loads.
+constexpr uint32_t kPrepThreads = 256;
+// CSR outliers of every row for all columns: y_csr[n][r] = sum over the row's
+// entries, in CSR order, of fp16(v) * x_n[perm[col]] (sparse_matvec,
+// outliers.cpp:131-141), exact fp32.  One thread per row; the row's entries
+// are loaded first so the x gathers of the columns are independent.
+__device__ __forceinline__ void csr_row(const float* __restrict__ xn, const uint16_t* __restrict__ perm,
+                                        const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ csr,
+                                        uint32_t rows, float* __restrict__ yn, uint32_t row) {
+  if (row >= rows) return;
+  const uint32_t e0 = __ldg(row_ptr + row), e1 = __ldg(row_ptr + row + 1);
+  float acc = 0.0f;
+  for (uint32_t e = e0; e < e1; e += 8) {
+    float p[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t ent = e + u < e1 ? __ldg(csr + e + u) : 0u;
+      p[u] = half_bits_to_float(ent >> 16) * __ldg(xn + __ldg(perm + (ent & 0xFFFFu)));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (e + u < e1) acc += p[u];
+  }
+  yn[row] = acc;
+}
+
+__global__ void __launch_bounds__(kPrepThreads) xprep_kernel(const float* __restrict__ x,
+                                                             const uint16_t* __restrict__ perm, Geometry G,
+                                                             uint32_t stages, uint32_t batch,
+                                                             uint16_t* __restrict__ xpt, int* __restrict__ xexp,
+                                                             uint32_t chunks, const uint32_t* __restrict__ row_ptr,
+                                                             const uint32_t* __restrict__ csr,
+                                                             float* __restrict__ ycsr) {
+  pdl_launch_dependents();  // the GEMM's weight stream does not depend on us
+  if (blockIdx.x >= chunks) {  // CSR blocks: one row of column blockIdx.y per thread
+    if (blockIdx.y < batch)
+      csr_row(x + (size_t)blockIdx.y * G.cols, perm, row_ptr, csr, G.rows, ycsr + (size_t)blockIdx.y * G.rows,
+              (blockIdx.x - chunks) * kPrepThreads + threadIdx.x);
+    return;
+  }
+  const uint32_t n = blockIdx.y;
+  const float* xn = x + (size_t)n * G.cols;
+  __shared__ float red[kPrepThreads / 32];
+  float m = 0.0f;
+  if (n < batch) {
+    const uint32_t n4v = G.cols >> 2;  // cols % 16 == 0 (validate_layer)
+    const float4* x4 = reinterpret_cast<const float4*>(xn);
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < n4v; i += kPrepThreads) {
+      const float4 v = __ldg(x4 + i);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = red[0];
+  for (int w = 1; w < (int)(kPrepThreads / 32); ++w) m = fmaxf(m, red[w]);
+  const int eb = (int)((__float_as_uint(m) >> 23) & 0xFFu);
+  const int e = (eb == 0 ? -126 : eb - 127) - 14;  // max |x'| in [2^14, 2^15)
+  if (threadIdx.x == 0 && blockIdx.x == 0) xexp[n] = e;
+  const uint32_t n2 = G.cols - G.n4;
+  const uint32_t i = blockIdx.x * kPrepThreads + threadIdx.x;
+  if (i >= stages * kStageK) return;
+  (void)n2;
+  const uint32_t st = i / kStageK, k = i % kStageK;
+  const uint32_t slot = k < 96 ? 96 * st + k : G.n2p + 32 * st + (k - 96);
+  float v = 0.0f;
+  if (n < batch && !(slot >= n2 && slot < G.n2p)) {
+    const int a = max(-126, min(127, -e));
+    v = __ldg(xn + perm[slot]) * p2(a) * p2(-e - a);
+  }
+  const uint32_t off = (k % 8) * 2 + (n % 8) * 16 + (n / 8) * 128 + (k / 8) * 256;
+  xpt[(size_t)st * (kBStageBytes / 2) + off / 2] = __half_as_ushort(__float2half_rn(v));
+}
+
+// ---------------------------------------------------------------- GEMM
+struct GemmArgs {
+  CUtensorMap tm[5];  // code2, meta, code4, s4, z4 boxes over [quads][dense_bytes]
+  CUtensorMap tso;    // sorder box: [row blocks of a tile][8 groups]
+  uint32_t so_rows;   // row blocks a tile spans (box height)
+  Geometry g;
+  const uint32_t* sorder;
+  const uint32_t* row_ptr;
+  const uint32_t* csr;
+  const uint16_t* perm;
+  const uint16_t* xpt;
+  const int* xexp;
+  const float* x;
+  float* y;
+  float* partial;
+  const float* ycsr;  // [batch][rows] CSR outlier sums (prologue kernel)
+  uint32_t* counters;
+  uint32_t batch, ks, stages, wstages;
+  int shift;
+  uint32_t rb_magic, rb_one;
+  unsigned long long* dbg;  // optional [grid][8] %globaltimer stamps
+};
+__device__ __forceinline__ void gstamp(const GemmArgs& a, uint32_t ev) {
+  if (a.dbg) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[blockIdx.x * 8 + ev] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const Geometry& G = a.g;
+  uint8_t* sA = smem;                                // kABufs x kATileBytes
+  uint8_t* sB = sA + kABufs * kATileBytes;           // kBSlots x 4 KB
+  uint8_t* sW = sB + kBSlots * kBStageBytes;         // kWSlots x 6656
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sW + kWSlots * kWStageBytes);
+  uint64_t* wfull = bars;              // [kWSlots]  TMA tx
+  uint64_t* wempty = wfull + kWSlots;  // [kWSlots]  8 dequant warps
+  uint64_t* bfull = wempty + kWSlots;  // [kBSlots]  TMA tx
+  uint64_t* bempty = bfull + kBSlots;  // [kBSlots]  tcgen05.commit
+  uint64_t* afull = bempty + kBSlots;  // [kABufs]   dequant warps
+  uint64_t* aempty = afull + kABufs;   // [kABufs]   tcgen05.commit
+  uint64_t* dfull = aempty + kABufs;   // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dfull + 1);
+  uint32_t* s_last = tmem_slot + 1;
+  float* s_dense = reinterpret_cast<float*>(s_last + 3);  // [128][17]
+
+  const uint32_t tile = blockIdx.x / a.ks, split = blockIdx.x % a.ks;
+  // K split over weight stages (8 tiles); sub-stages of 2 tiles feed the MMA
+  const uint32_t w0 = (uint32_t)((uint64_t)split * a.wstages / a.ks);
+  const uint32_t w1 = (uint32_t)((uint64_t)(split + 1) * a.wstages / a.ks);
+  const uint32_t nw = w1 - w0;
+  const uint32_t u0 = w0 * kSubPerW, u1 = min(w1 * kSubPerW, a.stages);
+  const uint32_t nsub = u1 - u0;  // sub-stages of this CTA
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t rb_tile = a.rb_one ? tile * kTileRows : __umulhi(tile * kTileRows, a.rb_magic);
+
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < kWSlots; ++i) mbar_init(&wfull[i], 1), mbar_init(&wempty[i], kDqWarps);
+    for (uint32_t i = 0; i < kBSlots; ++i) mbar_init(&bfull[i], 1), mbar_init(&bempty[i], 1);
+    for (uint32_t i = 0; i < kABufs; ++i) mbar_init(&afull[i], kDqWarps), mbar_init(&aempty[i], 1);
+    mbar_init(dfull, 1);
+    mbar_fence_init();
+  }
+  if (warp == 1) {  // TMEM: 32 columns (the 128 x 16 fp32 accumulator)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_addr(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) gstamp(a, 0);  // setup done
+
+  if (warp == 0) {
+    // ---------------- producer: weight boxes (8 tiles) + B tiles (per sub-stage)
+    if (lane == 0) {
+      const int qy = (int)(tile * kTileQuads);
+      auto load_w = [&](uint32_t i) {
+        const uint32_t wst = w0 + i, ws = i % kWSlots;
+        if (i >= kWSlots) mbar_wait(&wempty[ws], ((i / kWSlots) - 1) & 1u);
+        uint8_t* dst = sW + ws * kWStageBytes;
+        mbar_expect_tx(&wfull[ws], kOffSo + a.so_rows * kSoBoxG * 4);
+        tma_load_2d(dst + kOffC2, &a.tm[0], (int)(96 * wst), qy, &wfull[ws]);
+        tma_load_2d(dst + kOffMeta, &a.tm[1], (int)(G.off_meta / 4 + 16 * wst), qy, &wfull[ws]);
+        tma_load_2d(dst + kOffC4, &a.tm[2], (int)(G.off_c4 / 4 + 64 * wst), qy, &wfull[ws]);
+        tma_load_2d(dst + kOffS4, &a.tm[3], (int)(G.off_s4 / 4 + 16 * wst), qy, &wfull[ws]);
+        tma_load_2d(dst + kOffZ4, &a.tm[4], (int)(G.off_z4 / 4 + 4 * wst), qy, &wfull[ws]);
+        tma_load_2d(dst + kOffSo, &a.tso, (int)(24 * wst), (int)rb_tile, &wfull[ws]);
+      };
+      const uint32_t wpre = min(nw, kWSlots);
+      for (uint32_t i = 0; i < wpre; ++i) load_w(i);  // the weights do not depend on x
+      pdl_wait();  // B tiles are the prologue kernel's output
+      uint32_t wnext = wpre;
+      for (uint32_t i = 0; i < nsub; ++i) {
+        const uint32_t bs = i % kBSlots;
+        if (i >= kBSlots) mbar_wait(&bempty[bs], ((i / kBSlots) - 1) & 1u);
+        mbar_expect_tx(&bfull[bs], kBStageBytes);
+        bulk_load_nohint(sB + bs * kBStageBytes, a.xpt + (size_t)(u0 + i) * (kBStageBytes / 2), kBStageBytes,
+                         &bfull[bs]);
+        if ((i % kSubPerW) == 0 && wnext < nw) load_w(wnext++);
+      }
+      while (wnext < nw) load_w(wnext++);
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    if (lane == 0) {
+      for (uint32_t i = 0; i < nsub; ++i) {
+        const uint32_t ab = i % kABufs, ph = (i / kABufs) & 1u, bs = i % kBSlots;
+        mbar_wait(&afull[ab], ph);
+        mbar_wait(&bfull[bs], (i / kBSlots) & 1u);
+        if (i == 3) gstamp(a, 5);  // MMA thread: sub-stage 3's A and B ready
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t abase = smem_addr(sA + ab * kATileBytes), bbase = smem_addr(sB + bs * kBStageBytes);
+#pragma unroll
+        for (uint32_t kk = 0; kk < kStageK / 16; ++kk) {
+          const uint64_t da = umma_desc(abase + 2 * kk * kALbo, kALbo, kASbo);
+          const uint64_t db = umma_desc(bbase + kk * 512, 256, 128);
+          const uint32_t acc = (i | kk) ? 1u : 0u;
+          asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(tmem),
+                       "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_addr(&aempty[ab])));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_addr(&bempty[bs])));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_addr(dfull)));
+    }
+  } else {
+    // ---------------- dequant warps: item = (quad q, group j, channel half h) of a sub-stage
+    const uint32_t dt = threadIdx.x - 64, h = dt >> 8, q = (dt >> 3) & 31u, j = dt & 7u;
+    const uint32_t quad = tile * kTileQuads + q;
+    const uint32_t row0 = min(quad * 4, G.rows - 1);
+    const uint32_t rb_local = (a.rb_one ? row0 : __umulhi(row0, a.rb_magic)) - rb_tile;
+    const float s2sc = p2(12 - a.shift), s4sc = p2(9 - a.shift);
+    const uint32_t sub = j % 3;
+    const uint32_t esh = sub == 0 ? 6u : (sub == 1 ? 10u : 13u), emask = sub == 0 ? 15u : 7u;
+    const uint32_t eshl = sub == 0 ? 0u : 1u;
+    const uint32_t a_item = (q & 1u) * 8 + (q >> 1) * kASbo + (2 * j + h) * kALbo;  // + (c % 8) * 16
+    for (uint32_t i = 0; i < nsub; ++i) {
+      const uint32_t wi = i / kSubPerW, s4i = i % kSubPerW, ws = wi % kWSlots, ab = i % kABufs;
+      if (s4i == 0) mbar_wait(&wfull[ws], (wi / kWSlots) & 1u);
+      if (threadIdx.x == 64 && i == 3) gstamp(a, 1);  // sub-stage 3 weights present
+      const uint8_t* w = sW + ws * kWStageBytes;
+      uint32_t out[8][2];
+      if (j < 6) {
+        const uint32_t g6 = 6 * s4i + j;  // 2-bit group within the weight stage
+        const uint32_t sc = *reinterpret_cast<const uint32_t*>(w + kOffSo + (rb_local * kSoBoxG + g6) * 4);
+        const uint4 c = *reinterpret_cast<const uint4*>(w + kOffC2 + q * kBoxC2 * 4 + 16 * g6);
+        const uint2 m = *reinterpret_cast<const uint2*>(w + kOffMeta + q * kBoxMeta * 4 + 8 * (g6 / 3));
+        const half2 Sh = __float2half2_rn(half_bits_to_float(sc) * s2sc);  // scale2 2^(12-P)
+        const int zero2 = (int)(sc >> 16);
+        const uint32_t mm[2] = {m.x, m.y}, cw[2] = {h ? c.y : c.x, h ? c.w : c.z};
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const uint32_t v = mm[p];
+          const int mA = (int)(((v >> esh) & emask) << eshl) - zero2;
+          const int mB = (int)(((v >> (16 + esh)) & emask) << eshl) - zero2;
+          const int zA = (int)((v >> (2 * sub)) & 3u), zB = (int)((v >> (16 + 2 * sub)) & 3u);
+          half2 M[4];
+          M[0] = as_h2(pack_h2((float)mA * 4096.0f, (float)mB * 4096.0f));
+          M[1] = __hmul2(M[0], __float2half2_rn(0.25f));
+          M[2] = __hmul2(M[1], __float2half2_rn(0.25f));
+          M[3] = __hmul2(M[2], __float2half2_rn(0.25f));
+          const half2 Z = as_h2(pack_h2((float)(-zA * mA) * (1.0f / 4096.0f), (float)(-zB * mB) * (1.0f / 4096.0f)));
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const uint32_t src = cc < 4 ? cw[p] : cw[p] >> 8;
+            const int b = cc & 3;
+            const half2 t = as_h2(src & (0x00030003u << (2 * b)));
+            out[cc][p] = h2u(__hmul2(__hfma2(t, M[b], Z), Sh));
+          }
+        }
+      } else {
+        const uint32_t b2 = 2 * s4i + (j - 6);  // 4-bit block within the weight stage
+        const uint2 ca = *reinterpret_cast<const uint2*>(w + kOffC4 + q * kBoxC4 * 4 + 32 * b2 + 8 * h);
+        const uint2 cb = *reinterpret_cast<const uint2*>(w + kOffC4 + q * kBoxC4 * 4 + 32 * b2 + 16 + 8 * h);
+        const uint2 s4 = *reinterpret_cast<const uint2*>(w + kOffS4 + q * kBoxS4 * 4 + 8 * b2);
+        const uint32_t z4 = *reinterpret_cast<const uint16_t*>(w + kOffZ4 + q * kBoxZ4 * 4 + 2 * b2);
+        const uint32_t cw[2][2] = {{ca.x, ca.y}, {cb.x, cb.y}};
+        const uint32_t sw[2] = {s4.x, s4.y};
+        const half2 M0 = __float2half2_rn(32768.0f), M1 = __float2half2_rn(2048.0f);  // 2^(15-b)
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const float zA = (float)((z4 >> (8 * p)) & 15u), zB = (float)((z4 >> (8 * p + 4)) & 15u);
+          const half2 Z = as_h2(pack_h2(-zA * (1.0f / 512.0f), -zB * (1.0f / 512.0f)));
+          const half2 Sh = as_h2(pack_h2(half_bits_to_float(sw[p]) * s4sc, half_bits_to_float(sw[p] >> 16) * s4sc));
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const uint32_t word = cw[p][cc >> 2];
+            const int nib = cc & 3;
+            const uint32_t src = nib < 2 ? word : word >> 8;
+            const half2 t = as_h2(src & (0x000F000Fu << (4 * (nib & 1))));
+            out[cc][p] = h2u(__hmul2(__hfma2(t, (nib & 1) ? M1 : M0, Z), Sh));
+          }
+        }
+      }
+      if (s4i + 1 == kSubPerW || i + 1 == nsub) {  // last use of this weight slot
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wempty[ws]);
+      }
+      if (threadIdx.x == 64 && i == 3) gstamp(a, 2);  // sub-stage 3 decoded (registers)
+      if (i >= kABufs) mbar_wait(&aempty[ab], ((i / kABufs) - 1) & 1u);
+      if (threadIdx.x == 64 && i == 3) gstamp(a, 3);  // sub-stage 1's MMA done (A buffer free)
+      uint8_t* at = sA + ab * kATileBytes + a_item;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc)
+        *reinterpret_cast<uint2*>(at + cc * 16) = make_uint2(out[cc][0], out[cc][1]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&afull[ab]);
+      if (threadIdx.x == 64 && i == 3) gstamp(a, 4);  // sub-stage 3's A tile published
+    }
+    // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
+    if (warp < 6) {
+      mbar_wait(dfull, 0);
+      if (threadIdx.x == 64) gstamp(a, 7);  // accumulator ready
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t quarter = warp & 3u;
+      uint32_t r[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(tmem + ((quarter * 32u) << 16)));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      const uint32_t t = quarter * 32 + lane;  // row within the tile
+      pdl_wait();  // xexp is the prologue kernel's output
+#pragma unroll
+      for (int n = 0; n < 16; ++n) s_dense[t * 17 + n] = __uint_as_float(r[n]) * p2(a.shift + a.xexp[n]);
+    }
+  }
+  __syncthreads();
+
+  // dense part of this split is in s_dense[row][n] (row-major, padded stride 17)
+  if (a.ks == 1) {
+    // the dense sum, then the outliers (row_fma, engine.cpp:111-122): their
+    // per-row CSR sums (exact fp32, CSR order) come from the prologue kernel
+    pdl_wait();
+    for (uint32_t i = threadIdx.x; i < kTileRows * a.batch; i += blockDim.x) {
+      const uint32_t t = i % kTileRows, n = i / kTileRows, row = tile * kTileRows + t;
+      if (row < G.rows)
+        a.y[(size_t)n * G.rows + row] = s_dense[t * 17 + n] + __ldg(a.ycsr + (size_t)n * G.rows + row);
+    }
+  } else {
+    // split-K: the tile's K splits form one thread-block cluster; CTA `split`
+    // sums rows [split * 128 / ks, ...) over the splits' shared-memory
+    // partials (distributed shared memory) in split order -- deterministic
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    pdl_wait();
+    const uint32_t r0 = split * kTileRows / a.ks, r1 = (split + 1) * kTileRows / a.ks;
+    const uint32_t local = smem_addr(s_dense);
+    for (uint32_t i = threadIdx.x; i < (r1 - r0) * a.batch; i += blockDim.x) {
+      const uint32_t t = r0 + i % (r1 - r0), n = i / (r1 - r0), row = tile * kTileRows + t;
+      float s = 0.0f;
+      for (uint32_t sp = 0; sp < a.ks; ++sp) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + (t * 17 + n) * 4), "r"(sp));
+        float v;
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote));
+        s += v;
+      }
+      if (row < G.rows) a.y[(size_t)n * G.rows + row] = s + __ldg(a.ycsr + (size_t)n * G.rows + row);
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 0) gstamp(a, 6);  // y stored
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+}
+
+constexpr size_t kGemmSmem = 1024 + kABufs * kATileBytes + kBSlots * kBStageBytes + kWSlots * kWStageBytes + 512 +
+                             kTileRows * 17 * 4;
+static_assert(kGemmSmem <= 227 * 1024, "gemm shared memory");
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
+  const Geometry& G = L.g;
+  GemmPlan& p = L.gemm;
+  p = GemmPlan{};
+  // supported: paired tiles only (T2 == T4, even), 2-order blocks aligned to quads
+  if (G.T2 != G.T4 || G.T2 % 2 != 0 || G.T2 == 0 || G.group2 % kRowsPerQuad != 0) return 0;
+  auto enc = encode_fn();
+  if (!enc) return 0;
+  p.tiles = (G.rows + kTileRows - 1) / kTileRows;
+  p.stages = G.T2 / 2;                               // MMA sub-stages per row
+  p.wstages = (p.stages + kSubPerW - 1) / kSubPerW;  // weight stages per row
+  p.ks = std::max<uint32_t>(1, std::min<uint32_t>(std::min<uint32_t>(p.wstages, 8u), (uint32_t)num_sms / p.tiles));
+  // A = w 2^-P in fp16: scale2 2^(12-P) <= 2^15 and s4 2^(9-P) <= 2^15
+  int P = -126;
+  if (max_scale2 > 0.0f && std::isfinite(max_scale2)) P = std::max(P, std::ilogb(max_scale2) - 2);
+  if (max_s4 > 0.0f && std::isfinite(max_s4)) P = std::max(P, std::ilogb(max_s4) - 5);
+  p.shift = std::max(-100, std::min(100, P == -126 ? 0 : P));
+  const uint32_t boxw[5] = {kBoxC2, kBoxMeta, kBoxC4, kBoxS4, kBoxZ4};
+  for (int f = 0; f < 5; ++f) {
+    cuuint64_t dims[2] = {G.dense_bytes / 4, G.quads};
+    cuuint64_t strides[1] = {G.dense_bytes};
+    cuuint32_t box[2] = {boxw[f], kTileQuads};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(reinterpret_cast<CUtensorMap*>(p.tmap[f]), CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, L.quads, dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return 0;
+  }
+  {  // sorder [row_blocks][G2s] u32, box [so_rows][8 groups]
+    p.so_rows = (kTileRows + G.group2 - 1) / G.group2 + (kTileRows % G.group2 ? 1u : 0u);
+    if (p.so_rows > kSoRowsMax) return 0;
+    cuuint64_t dims[2] = {G.G2s, G.row_blocks};
+    cuuint64_t strides[1] = {(cuuint64_t)G.G2s * 4};
+    cuuint32_t box[2] = {kSoBoxG, p.so_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(reinterpret_cast<CUtensorMap*>(p.tmap_so), CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, L.sorder, dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return 0;
+  }
+  cudaError_t e;
+  if ((e = cudaMalloc((void**)&p.partial, (size_t)p.ks * 16 * G.rows * 4 + 16)) != cudaSuccess) return (int)e;
+  if ((e = cudaMalloc((void**)&p.counters, (size_t)p.tiles * 4)) != cudaSuccess) return (int)e;
+  if ((e = cudaMemset(p.counters, 0, (size_t)p.tiles * 4)) != cudaSuccess) return (int)e;
+  if ((e = cudaMalloc((void**)&p.xpt, (size_t)p.stages * kBStageBytes)) != cudaSuccess) return (int)e;
+  if ((e = cudaMalloc((void**)&p.xexp, 16 * sizeof(int))) != cudaSuccess) return (int)e;
+  if ((e = cudaMalloc((void**)&p.ycsr, (size_t)16 * G.rows * 4)) != cudaSuccess) return (int)e;
+  static bool attr = false;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem)) !=
+        cudaSuccess)
+      return (int)e;
+    if ((e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+      return (int)e;
+    attr = true;
+  }
+  p.ok = 1;
+  return 0;
+}
+
+void free_gemm(DeviceLayer& L) {
+  GemmPlan& p = L.gemm;
+  cudaFree(p.partial), cudaFree(p.counters), cudaFree(p.xpt), cudaFree(p.xexp), cudaFree(p.ycsr);
+  p.partial = nullptr, p.counters = nullptr, p.xpt = nullptr, p.xexp = nullptr, p.ycsr = nullptr;
+  p.ok = 0;
+}
+
+int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream,
+                unsigned long long* dbg) {
+  const Geometry& G = L.g;
+  const GemmPlan& p = L.gemm;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t chunks = (p.stages * kStageK + kPrepThreads - 1) / kPrepThreads;
+  const uint32_t csr_blocks = (G.rows + kPrepThreads - 1) / kPrepThreads;
+  xprep_kernel<<<dim3(chunks + csr_blocks, 16), kPrepThreads, 0, st>>>(x, L.perm16, G, p.stages, batch, p.xpt,
+                                                                       p.xexp, chunks, L.row_ptr, L.csr, p.ycsr);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  GemmArgs a;
+  std::memcpy(a.tm, p.tmap, sizeof(a.tm));
+  std::memcpy(&a.tso, p.tmap_so, sizeof(a.tso));
+  a.so_rows = p.so_rows;
+  a.g = G;
+  a.sorder = L.sorder, a.row_ptr = L.row_ptr, a.csr = L.csr, a.perm = L.perm16;
+  a.xpt = p.xpt, a.xexp = p.xexp, a.x = x, a.y = y;
+  a.partial = p.partial, a.counters = p.counters, a.ycsr = p.ycsr;
+  a.batch = batch, a.ks = p.ks, a.stages = p.stages, a.wstages = p.wstages, a.shift = p.shift;
+  a.rb_magic = L.plan.rb_magic, a.rb_one = L.plan.rb_one;
+  a.dbg = dbg;
+  // cluster = the tile's K splits (DSMEM reduction); PDL: the weight stream
+  // starts while the prologue runs, B tiles / scales wait for it
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.tiles * p.ks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kGemmSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.ks, attr[0].val.clusterDim.y = 1, attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  void* params[] = {&a};
+  return (int)cudaLaunchKernelExC(&cfg, (const void*)gemm_kernel, params);
+}
+
+}  // namespace qwdev

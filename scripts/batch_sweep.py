@@ -1,0 +1,49 @@
+"""BASELINE config 3: Llama-2-7B shapes, batch 1/2/4/8/16 (K2 for b = 1, K4 for b >= 2).
+Per-call time from a CUDA-graph chain of N distinct layer copies (inputs > L2).
+usage: python scripts/batch_sweep.py [N]  -> one JSON line per (shape, batch)"""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2311_16442_b200 as qw  # noqa: E402
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+out = []
+for name, rows, cols in (("q_proj", 4096, 4096), ("gate_proj", 11008, 4096), ("down_proj", 4096, 11008)):
+    layer = qw.synth_layer(rows, cols, seed=7)
+    base = qw.DeviceLayer(layer)
+    dls = [base] + [base.clone() for _ in range(N - 1)]
+    payload = qw.payload_bytes(layer)
+    for b in (1, 2, 4, 8, 16):
+        xs = torch.from_numpy(np.stack([qw.synth_activation(cols, 50 + i) for i in range(b)])).cuda()
+        ys = torch.empty(N, b, rows, device="cuda")
+
+        def run():
+            for i, d in enumerate(dls):
+                d.matvec(xs, out=ys[i], pdl=(b == 1))
+        run()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            run()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        R = 10
+        for _ in range(R):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (R * N)
+        balg = payload + 4 * b * (rows + cols)
+        line = {"shape": name, "rows": rows, "cols": cols, "batch": b, "us_per_call": round(us, 3),
+                "gb_s": round(balg / us / 1e3, 1), "tflops": round(2 * b * rows * cols / us / 1e6, 2),
+                "path": "K2 fused GEMV" if b == 1 else "K4 tcgen05 GEMM",
+                "launches": base.launches_per_matvec(b)}
+        print(json.dumps(line), flush=True)

@@ -176,3 +176,45 @@ def test_llama7b_shapes(rows, cols):
     x = qw.synth_activation(cols, 8)
     err, _ = check_layer(layer, x)
     assert err < 2e-3
+
+
+# ---------------------------------------------------------------- K4 (batched)
+BATCH_GEOMS = [
+    # rows, cols, batch: tensor-core path (paired tiles, group2 % 4 == 0)
+    (96, 512, 2),       # one partial M tile
+    (300, 1024, 5),     # 3 tiles, last partial; rows % 4 == 0
+    (130, 768, 16),     # rows % 4 != 0 inside the last tile, full batch
+    (512, 4096, 8),     # K split across CTAs (split-K fixup)
+    (4096, 4096, 16),   # Llama-2-7B q_proj, batch 16
+]
+
+
+@pytest.mark.parametrize("rows,cols,batch", BATCH_GEOMS)
+def test_batched_tensor_core_path(rows, cols, batch):
+    torch = _torch()
+    layer = qw.synth_layer(rows, cols, seed=rows + cols + batch, outlier_ratio=0.005)
+    dl = qw.DeviceLayer(layer)
+    assert dl.launches_per_matvec(batch) == 2, "expected x prologue + tcgen05 GEMM"
+    xs = np.stack([qw.synth_activation(cols, 300 + b) for b in range(batch)])
+    Y = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
+    assert np.all(np.isfinite(Y))
+    for b in range(batch):
+        ref = oracle.matvec_f64(layer, xs[b])
+        err = rel_l2(Y[b], ref)
+        assert err <= TOL, (b, err)
+        assert np.max(np.abs(Y[b] - ref)) <= TOL * np.max(np.abs(ref))
+    # deterministic run to run (fixed split-K summation order)
+    Y2 = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
+    assert np.array_equal(Y, Y2)
+
+
+def test_batched_unsupported_geometry_falls_back_to_columns():
+    """Unpaired tiles (T2 != T4) keep the per-column fused GEMV (still exact semantics)."""
+    torch = _torch()
+    layer = qw.synth_layer(24, 160, seed=4, alpha=0.5)
+    dl = qw.DeviceLayer(layer)
+    assert dl.launches_per_matvec(3) == 3
+    xs = np.stack([qw.synth_activation(160, 40 + b) for b in range(3)])
+    Y = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
+    for b in range(3):
+        assert rel_l2(Y[b], oracle.matvec_f64(layer, xs[b])) <= TOL
