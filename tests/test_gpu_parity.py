@@ -218,3 +218,23 @@ def test_batched_unsupported_geometry_falls_back_to_columns():
     Y = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
     for b in range(3):
         assert rel_l2(Y[b], oracle.matvec_f64(layer, xs[b])) <= TOL
+
+
+# ---------------------------------------------------------------- TP (1 rank over NCCL)
+@pytest.mark.parametrize("mode", ["col", "row"])
+def test_tp_linear_single_rank_nccl(mode):
+    """The TP shard + NCCL collective path on one GPU (world size 1): the
+    GPU code path end to end; multi-rank semantics are tested with gloo."""
+    import os
+    import torch.distributed as dist
+    torch = _torch()
+    from paper_2311_16442_b200.tp import TPLinear
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    layer = qw.synth_layer(256, 1024, seed=9, outlier_ratio=0.005)
+    x = qw.synth_activation(1024, 10)
+    tp = TPLinear(layer, 0, 1, mode, device="cuda:0")
+    y = tp.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel_l2(y, oracle.matvec_f64(layer, x)) <= TOL
