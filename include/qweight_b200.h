@@ -180,6 +180,15 @@ int qw_matvec_pdl(const qw_layer* layer, const float* x, uint32_t batch,
                                       reading it (q/k/v, gate/up share inputs) */
 int qw_matvec_ex(const qw_layer* layer, const float* x, uint32_t batch, float* y,
                  qw_workspace* ws, void* stream, uint32_t flags);
+/* Group launch (batch 1): up to 4 layers with identical geometry that read
+ * the same activation (q/k/v, gate/up) in ONE fused launch -- one dependency
+ * wait, one activation staging.  The layers must outlive the group.
+ * ys[i]: device fp32 [rows] output of layers[i]. */
+typedef struct qw_group qw_group;
+int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out);
+int qw_group_free(qw_group* group);
+int qw_group_matvec(const qw_group* group, const float* x, float* const* ys, void* stream,
+                    uint32_t flags);
 /* Host-buffer, synchronous, checked: length and finiteness as the reference
  * (engine.cpp:124-132).  x_len must equal batch * cols. */
 int qw_matvec_host(const qw_layer* layer, const float* x, uint64_t x_len,

@@ -43,7 +43,14 @@ struct qw_layer {
   int device = 0;
   int num_sms = 148;
   float max_scale2 = 0.0f, max_s4 = 0.0f;  // for the batched path's fp16 range
+  std::vector<uint32_t> host_row_ptr;       // CSR row pointers (group launch plans)
   qw_layer_info info{};
+};
+
+struct qw_group {
+  qwdev::GemvPlan plan;
+  std::vector<const qwdev::DeviceLayer*> layers;  // borrowed
+  int device = 0;
 };
 
 struct qw_workspace {
@@ -508,7 +515,9 @@ int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
     std::vector<uint16_t> perm16(L.plan.perm.size());
     for (size_t i = 0; i < perm16.size(); ++i)
       perm16[i] = L.plan.perm[i] == qwb::kPad ? 0 : (uint16_t)L.plan.perm[i];
-    if (int pe = qwdev::plan_gemv(H->dev, H->num_sms, L.csr.row_ptr.data())) {
+    H->host_row_ptr = L.csr.row_ptr;
+    if (H->host_row_ptr.empty()) H->host_row_ptr.assign((size_t)L.cfg.rows + 1, 0u);
+    if (int pe = qwdev::plan_gemv(H->dev, H->num_sms, H->host_row_ptr.data())) {
       if (pe == (int)cudaErrorInvalidConfiguration)
         return fail(QW_ERR_UNSUPPORTED, "upload: layer too wide for the fused GEMV (at most 60 "
                                         "chunks of 32 groups, i.e. about 30720 input channels)");
@@ -685,6 +694,7 @@ int qw_layer_clone(const qw_layer* L, qw_layer** out) {
     return cuda_fail(e, "clone");
   }
   H->max_scale2 = L->max_scale2, H->max_s4 = L->max_s4;
+  H->host_row_ptr = L->host_row_ptr;
   H->dev.gemm = qwdev::GemmPlan{};
   if (int ge = qwdev::plan_gemm(H->dev, H->num_sms, H->max_scale2, H->max_s4)) {
     free_dev(H->dev);
@@ -701,6 +711,47 @@ int qw_debug_timeline(const qw_layer* L, const float* x, float* y, unsigned long
   const int e = qwdev::launch_gemv(L->dev, x, 1, y, stream, flags & 1u, stamps, repeat,
                                    (flags & 2u) != 0, (flags & 4u) ? qwdev::kXIndependent : 0u);
   return e ? cuda_fail((cudaError_t)e, "gemv launch") : QW_OK;
+}
+
+int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out) {
+  return guarded([&] {
+    if (!layers || !out || n == 0) return fail(QW_ERR_ARG, "group: null argument");
+    if (n > qwdev::kMaxSeg) return fail(QW_ERR_UNSUPPORTED, "group: at most 4 layers");
+    auto G = std::make_unique<qw_group>();
+    std::vector<const uint32_t*> rps;
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!layers[i]) return fail(QW_ERR_ARG, "group: null layer");
+      if (layers[i]->device != layers[0]->device) return fail(QW_ERR_ARG, "group: layers on different devices");
+      G->layers.push_back(&layers[i]->dev);
+      rps.push_back(layers[i]->host_row_ptr.data());
+    }
+    G->device = layers[0]->device;
+    cudaSetDevice(G->device);
+    const int e = qwdev::plan_gemv_group(G->plan, G->layers.data(), rps.data(), n, layers[0]->num_sms);
+    if (e == (int)cudaErrorInvalidValue)
+      return fail(QW_ERR_ARG, "group: layers must share rows, cols, channel split and group2");
+    if (e) return cuda_fail((cudaError_t)e, "group plan");
+    *out = G.release();
+    return (int)QW_OK;
+  });
+}
+
+int qw_group_free(qw_group* g) {
+  delete g;
+  return QW_OK;
+}
+
+int qw_group_matvec(const qw_group* g, const float* x, float* const* ys, void* stream, uint32_t flags) {
+  if (!g || !x || !ys) return fail(QW_ERR_ARG, "group matvec: null argument");
+  for (size_t i = 0; i < g->layers.size(); ++i)
+    if (!ys[i]) return fail(QW_ERR_ARG, "group matvec: null output");
+  int dev_now = -1;
+  cudaGetDevice(&dev_now);
+  if (dev_now != g->device) cudaSetDevice(g->device);
+  const int e = qwdev::launch_gemv_group(g->plan, g->layers.data(), (uint32_t)g->layers.size(), x, ys, stream,
+                                         (flags & QW_LAUNCH_PDL) != 0,
+                                         (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u);
+  return e ? cuda_fail((cudaError_t)e, "group launch") : QW_OK;
 }
 
 int qw_debug_gemm_timeline(const qw_layer* L, const float* x, uint32_t batch, float* y,

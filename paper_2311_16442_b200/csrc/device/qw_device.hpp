@@ -49,8 +49,16 @@ struct GemvPlan {
   float s_scale = 1.0f;  // 2^-P applied to 2-bit s1 so 15 * max scale2 * 2^-P fits fp16
   uint32_t so_off = 0, part_off = 0, xg_off = 0, misc_off = 0, win_off = 0, pre_off = 0, bar_off = 0;  // smem layout
   uint32_t smem = 0;
-  uint32_t csr_lo[kMaxGrid + 1] = {};  // first CSR entry of each CTA's rows
+  // per CTA: layer (segment) of a group launch, quad range, CSR entry range
+  uint8_t cta_seg[kMaxGrid] = {};
+  uint32_t cta_q0[kMaxGrid] = {}, cta_q1[kMaxGrid] = {}, cta_e0[kMaxGrid] = {}, cta_e1[kMaxGrid] = {};
 };
+
+// A group launch: up to kMaxSeg layers of identical geometry that read the
+// same activation (q/k/v, gate/up); the CTAs are split across the layers in
+// proportion to their quads and each CTA owns a quad range of one layer, so
+// the dependency wait, the activation staging and the launch are paid once.
+constexpr uint32_t kMaxSeg = 4;
 
 // Batched (2..16 columns) tensor-core plan: 128-row M tiles x KS K splits of
 // 2-tile stages (96 2-bit + 32 4-bit channels); TMA 2-D boxes of the quad
@@ -92,6 +100,12 @@ struct Workspace {
 // Launchers (return cudaError_t as int).
 // Fill L.plan for a device with num_sms SMs (returns cudaError_t).
 int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr);
+// Plan a group launch over layers[0..n) (identical geometry); returns
+// cudaError_t, cudaErrorInvalidValue when the geometries differ.
+int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_t* const* host_row_ptrs,
+                    uint32_t n, int num_sms);
+int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
+                      float* const* ys, void* stream, bool pdl, uint32_t flags);
 // y[col] = W_q x[col] for col < batch: one fused kernel per column.
 constexpr uint32_t kTimelineEvents = 12;  // entry, copies issued, prologue, first quad, consumers, y, csr
 // flags: kXIndependent = x was not written by the preceding kernel on the

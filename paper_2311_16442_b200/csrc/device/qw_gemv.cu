@@ -144,24 +144,26 @@ __device__ __forceinline__ uint32_t pack_h2(float2 v) {  // cvt.rn.f16x2.f32
 
 // ------------------------------------------------------------ K2+K3 GEMV
 struct GemvArgs {
-  const uint8_t* quads;
-  const uint32_t* sorder;
-  const uint32_t* row_ptr;
-  const uint32_t* csr;
-  const uint16_t* perm;
+  // per layer (segment) of the launch
+  const uint8_t* quads[kMaxSeg];
+  const uint32_t* sorder[kMaxSeg];
+  const uint32_t* row_ptr[kMaxSeg];
+  const uint32_t* csr[kMaxSeg];
+  const uint16_t* perm[kMaxSeg];
+  float* y[kMaxSeg];
+  float s_scale[kMaxSeg];  // 2^-P: keeps (eff - zero2) scale2 2^-P inside fp16
   const float* x;
-  float* y;
   Geometry g;
   uint32_t W, W2, S, grid, nq_max;
   uint32_t rb_magic, rb_one;  // row / group2 = rb_one ? row : umulhi(row, rb_magic)
-  float s_scale;              // 2^-P: keeps (eff - zero2) scale2 2^-P inside fp16
   uint32_t repeat;  // diagnostics: consumers re-run the resident quads this many times
   uint32_t wait_x;  // x is the previous kernel's output: griddepcontrol.wait before reading it
   uint32_t pre;     // precompute 1st-order scales of resident units before x
   uint32_t so_off, part_off, csr_off, x_off, win_off, pre_off, bar_off;
   unsigned long long* dbg;  // optional timeline: kTimelineEvents stamps per CTA
   uint32_t dbg_global;      // stamps from %globaltimer (ns) instead of clock64
-  uint32_t csr_lo[kMaxGrid + 1];
+  uint8_t cta_seg[kMaxGrid];
+  uint32_t cta_q0[kMaxGrid], cta_q1[kMaxGrid], cta_e0[kMaxGrid], cta_e1[kMaxGrid];
 };
 
 __device__ __forceinline__ void stamp_impl(const GemvArgs& a, uint32_t ev) {
@@ -207,9 +209,16 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
   uint64_t* s_sobar = s_empty + S;
   uint64_t* s_xbar = s_sobar + 1;
 
-  const uint32_t q0 = (uint32_t)((uint64_t)blockIdx.x * G.quads / a.grid);
-  const uint32_t q1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * G.quads / a.grid);
+  const uint32_t seg = a.cta_seg[blockIdx.x];
+  const uint32_t q0 = a.cta_q0[blockIdx.x], q1 = a.cta_q1[blockIdx.x];
   const uint32_t nq = q1 - q0;
+  const uint8_t* __restrict__ g_quads = a.quads[seg];
+  const uint32_t* __restrict__ g_sorder = a.sorder[seg];
+  const uint32_t* __restrict__ g_row_ptr = a.row_ptr[seg];
+  const uint32_t* __restrict__ g_csr = a.csr[seg];
+  const uint16_t* __restrict__ g_perm = a.perm[seg];
+  float* __restrict__ g_y = a.y[seg];
+  const float s_scale = a.s_scale[seg];
   const uint32_t nunit = (nq + NQ - 1) / NQ;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t r_begin = q0 * kRowsPerQuad;
@@ -234,11 +243,11 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
       const uint32_t so_bytes = nrows ? (row_block(r_end - 1) - rb_first + 1) * G.G2s * 4u : 0u;
       if (so_bytes) {
         mbar_expect_tx(s_sobar, so_bytes);
-        bulk_load_nohint(smem + a.so_off, a.sorder + (size_t)rb_first * G.G2s, so_bytes, s_sobar);
+        bulk_load_nohint(smem + a.so_off, g_sorder + (size_t)rb_first * G.G2s, so_bytes, s_sobar);
       } else {
         mbar_arrive(s_sobar);
       }
-      const uint8_t* src = a.quads + (size_t)q0 * dense;
+      const uint8_t* src = g_quads + (size_t)q0 * dense;
       const uint32_t npre = min(nunit, S);
       uint32_t slot = 0, phase = 0;
       for (uint32_t u = 0; u < nunit; ++u) {
@@ -267,8 +276,8 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
 
   if (warp == W + 1) {
     // ================= outliers: exact fp32 x, CSR order within a row
-    const uint32_t e_lo = a.csr_lo[blockIdx.x], e_hi = a.csr_lo[blockIdx.x + 1];
-    for (uint32_t t = lane; t <= nrows; t += 32) s_rp[t] = a.row_ptr[r_begin + t] - e_lo;
+    const uint32_t e_lo = a.cta_e0[blockIdx.x], e_hi = a.cta_e1[blockIdx.x];
+    for (uint32_t t = lane; t <= nrows; t += 32) s_rp[t] = g_row_ptr[r_begin + t] - e_lo;
     for (uint32_t t = lane; t < nrows; t += 32) s_csr[t] = 0.0f;
     const uint32_t n = e_hi - e_lo;
     constexpr int kPer = 8;
@@ -277,10 +286,10 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
         const uint32_t e = c0 + lane + 32u * j;
-        ent[j] = e < n ? __ldg(a.csr + e_lo + e) : 0u;
+        ent[j] = e < n ? __ldg(g_csr + e_lo + e) : 0u;
       }
 #pragma unroll
-      for (int j = 0; j < kPer; ++j) src[j] = __ldg(a.perm + (ent[j] & 0xFFFFu));
+      for (int j = 0; j < kPer; ++j) src[j] = __ldg(g_perm + (ent[j] & 0xFFFFu));
     };
     if (n) fetch(0);
     __syncwarp();
@@ -374,7 +383,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
         for (int i = 0; i < (UNI ? 1 : 4); ++i) {
           const uint32_t rb = row_block(min(r0 + i, G.rows - 1)) - rb_first;
           const uint32_t e = s_so[rb * G.G2s + gk[k]];
-          const float A = half_bits_to_float(e) * a.s_scale;  // exact: scale2 * 2^-P
+          const float A = half_bits_to_float(e) * s_scale;  // exact: scale2 * 2^-P
           Ae[j][k][i] = A * pow2f(24 - pe[k]);
           Bz[j][k][i] = -small_int_to_float(e >> 16) * A;
         }
@@ -415,13 +424,15 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
       }
     }
 
-    // ---- activation prologue: layer-wide power-of-two scale (max|x'| in
-    // [2^10, 2^11): every fp16 x' keeps 11 bits and the group sums of |x'|
-    // stay < 2^15), gather the lane's groups in permuted order.
+    // ---- activation prologue: gather the lane's groups in permuted order and
+    // scale them by a per-warp power of two (max|x'| in [2^10, 2^11): every
+    // fp16 x' keeps 11 bits, the group sums of |x'| stay < 2^15).  The warp's
+    // row sums share that scale, undone once per row in the reduction window,
+    // so no CTA-wide reduction sits on the critical path.
     uint32_t pw[KG][8];
 #pragma unroll
     for (int k = 0; k < KG; ++k) {
-      const uint4* pp = reinterpret_cast<const uint4*>(a.perm + 16u * gk[k]);
+      const uint4* pp = reinterpret_cast<const uint4*>(g_perm + 16u * gk[k]);
       const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
       pw[k][0] = p0.x, pw[k][1] = p0.y, pw[k][2] = p0.z, pw[k][3] = p0.w;
       pw[k][4] = p1.x, pw[k][5] = p1.y, pw[k][6] = p1.z, pw[k][7] = p1.w;
@@ -436,46 +447,56 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
       if (a.wait_x) pdl_wait();  // x is the previous kernel's output
       xs = a.x;
     }
-    float mx = 0.0f;
-    for (uint32_t i = threadIdx.x * 4; i < G.cols; i += W * 128) {
-      const float4 v = XSM ? *reinterpret_cast<const float4*>(xs + i)
-                           : __ldg(reinterpret_cast<const float4*>(xs + i));
-      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    if (lane == 0) s_red[warp] = mx;
-    named_sync(1, W * 32);
-    mx = s_red[0];
-    for (uint32_t w2 = 1; w2 < W; ++w2) mx = fmaxf(mx, s_red[w2]);
-    if (threadIdx.x == 0) stamp(a.dbg, 9);  // layer-wide max known
-    const int eb = (int)((__float_as_uint(mx) >> 23) & 0xFFu);
-    const int sh = (eb == 0 ? -126 : eb - 127) - 10;  // floor(log2 max) - 10
     const uint32_t n2 = G.cols - G.n4;
-    half2 X[KG][16], nsxh[KG];
+    float xv[KG][16];
+    float mx = 0.0f;
 #pragma unroll
     for (int k = 0; k < KG; ++k) {
-      const uint32_t g = gk[k], s0 = 16u * g;
-      float sx = 0.0f;
+      const uint32_t s0 = 16u * gk[k];
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj) {
         const uint32_t c = (pw[k][jj >> 1] >> (16 * (jj & 1))) & 0xFFFFu;
         float v = XSM ? xs[c] : __ldg(xs + c);
         if (TWO && s0 + jj >= n2 && s0 + jj < G.n2p) v = 0.0f;  // pads (apply_permutation)
         if (!lv[k]) v = 0.0f;
-        const int b = TWO ? 2 * (jj & 3) : 4 * (jj & 1);
-        const int e = -sh - b;
-        const int e1 = max(-126, min(127, e));
-        const __half h = __float2half_rn(v * pow2f(e1) * pow2f(max(-126, min(127, e - e1))));
-        X[k][jj] = __half2half2(h);
-        sx += __half2float(h) * pow2f(b - 24);
+        xv[k][jj] = v;
+        mx = fmaxf(mx, fabsf(v));
+      }
+    }
+    // one scale per warp (a shuffle reduction, no CTA barrier): the row sums
+    // of a warp's lanes then share it and it is undone once per row
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (threadIdx.x == 0) stamp(a.dbg, 9);  // gathered
+    const int eb = (int)((__float_as_uint(mx) >> 23) & 0xFFu);
+    const int sh = (eb == 0 ? -126 : eb - 127) - 10;  // floor(log2 max) - 10
+    // x' 2^-b as two normal power-of-two factors (any finite x), b = bit position
+    float f1[4], f2[4];
+#pragma unroll
+    for (int bi = 0; bi < 4; ++bi) {
+      const int e = -sh - (TWO ? 2 * bi : 4 * bi);
+      const int e1 = max(-126, min(127, e));
+      f1[bi] = pow2f(e1), f2[bi] = pow2f(max(-126, min(127, e - e1)));
+    }
+    half2 X[KG][16], nsxh[KG];
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      const uint32_t g = gk[k];
+      float sx = 0.0f;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int bi = TWO ? (jj & 3) : (jj & 1);
+        const int b = TWO ? 2 * bi : 4 * bi;
+        const __half hh = __float2half_rn(xv[k][jj] * f1[bi] * f2[bi]);
+        X[k][jj] = __half2half2(hh);
+        sx += __half2float(hh) * pow2f(b - 24);
       }
       // zero point: z lands at 2^(2 sub - 24) (2-bit) or 2^-24 (4-bit): z_h nsxh = -z sum x'
       const int zp = TWO ? 2 * (int)(g - 3u * (g / 3u)) : 0;
       nsxh[k] = __float2half2_rn(-sx * pow2f(24 - zp));
     }
     // every accumulated term is in units of 2^(sh + 24) (and 2^P for 2-bit s1)
-    const float yscale = pow2f(max(-126, min(127, sh + 24))) * (TWO ? 1.0f / a.s_scale : 1.0f);
+    const float yscale = pow2f(max(-126, min(127, sh + 24))) * (TWO ? 1.0f / s_scale : 1.0f);
     if (threadIdx.x == 0) stamp(a.dbg, 2);  // prologue done
     if (threadIdx.x == 0 && a.dbg && nunit) {  // diagnostics: the first unit is in
       mbar_wait(&s_full[0], 0);
@@ -588,7 +609,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
     const float* p = s_part + t * W;
     float s = p[0];
     for (uint32_t w2 = 1; w2 < W; ++w2) s += p[w2];
-    a.y[r_begin + t] = s + s_csr[t];
+    g_y[r_begin + t] = s + s_csr[t];
   }
   if (threadIdx.x == 0) stamp(a.dbg, 5);
 }
@@ -639,14 +660,14 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
 
-int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
-  const Geometry& G = L.g;
-  GemvPlan& p = L.plan;
+namespace {
+// geometry-dependent part of a plan (warps, groups per lane, quads per slot, ...)
+int plan_geometry(GemvPlan& p, const Geometry& G) {
   // chunks of 32 groups, kept apart per type so each warp is all 2-bit or all 4-bit
   const uint32_t c2 = (G.G2 + 31u) / 32u, c4 = (G.T4 + 31u) / 32u;
   p.nchunks = c2 + c4;
-  // lanes own KG groups of every quad, W warps cover a row: W <= 12 (KG 1 when
-  // a row is at most 12 chunks, else the fewest KG <= 4 with W <= 16)
+  // lanes own KG groups of every quad, W warps cover a row: W <= 8 for KG <= 2
+  // (two CTAs per SM), else the fewest KG <= 4 with W <= 15
   auto warps_for = [&](uint32_t kg) { return (c2 + kg - 1) / kg + (c4 + kg - 1) / kg; };
   p.kmax = 1;
   while (p.kmax < 4 && warps_for(p.kmax) > (p.kmax <= 2 ? 8u : 15u)) ++p.kmax;
@@ -654,22 +675,34 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
   p.warps = warps_for(p.kmax);
   p.warps2 = (c2 + p.kmax - 1) / p.kmax;
   p.teams = 1;
-  uint32_t per_sm = 1;
-  if (const char* e = std::getenv("QW_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
-  p.grid = std::min<uint32_t>(std::min<uint32_t>((uint32_t)num_sms * per_sm, kMaxGrid), G.quads);
-  p.nq_max = (G.quads + p.grid - 1) / p.grid;
   p.uniform_rb = (G.group2 % kRowsPerQuad) == 0;
   p.uq = quads_per_slot(p.kmax, p.uniform_rb);
   p.xsm = G.cols <= 12288;
   p.rb_one = G.group2 == 1;
   p.rb_magic = p.rb_one ? 0u : (uint32_t)((0x100000000ull + G.group2 - 1) / G.group2);
-  uint32_t so_rows_max = 0;
-  for (uint32_t b = 0; b <= p.grid; ++b) {
-    const uint32_t q = (uint32_t)((uint64_t)b * G.quads / p.grid);
-    p.csr_lo[b] = host_row_ptr[std::min(q * (uint32_t)kRowsPerQuad, G.rows)];
-    if (b < p.grid) {
-      const uint32_t qn = (uint32_t)((uint64_t)(b + 1) * G.quads / p.grid);
-      const uint32_t r0 = q * kRowsPerQuad, r1 = std::min(qn * kRowsPerQuad, G.rows);
+  return 0;
+}
+
+// CTA ranges (one layer each) + shared-memory layout for the largest range
+int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_ptrs, uint32_t n, int num_sms) {
+  uint32_t per_sm = 1;
+  if (const char* e = std::getenv("QW_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
+  const uint64_t total = (uint64_t)n * G.quads;
+  uint32_t grid = (uint32_t)std::min<uint64_t>(std::min<uint32_t>((uint32_t)num_sms * per_sm, kMaxGrid), total);
+  grid = std::max(grid, n);
+  p.grid = grid;
+  p.nq_max = 0;
+  uint32_t so_rows_max = 0, cta = 0;
+  for (uint32_t l = 0; l < n; ++l) {
+    const uint32_t g_l = grid * (l + 1) / n - grid * l / n;  // CTAs of layer l
+    for (uint32_t b = 0; b < g_l; ++b, ++cta) {
+      const uint32_t q0 = (uint32_t)((uint64_t)b * G.quads / g_l), q1 = (uint32_t)((uint64_t)(b + 1) * G.quads / g_l);
+      p.cta_seg[cta] = (uint8_t)l;
+      p.cta_q0[cta] = q0, p.cta_q1[cta] = q1;
+      const uint32_t r0 = q0 * kRowsPerQuad, r1 = std::min(q1 * kRowsPerQuad, G.rows);
+      p.cta_e0[cta] = host_row_ptrs[l][std::min(r0, G.rows)];
+      p.cta_e1[cta] = host_row_ptrs[l][std::min(r1, G.rows)];
+      p.nq_max = std::max(p.nq_max, q1 - q0);
       if (r1 > r0) so_rows_max = std::max(so_rows_max, (r1 - 1) / G.group2 - r0 / G.group2 + 1);
     }
   }
@@ -688,12 +721,12 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
   const size_t units = (p.nq_max + p.uq - 1) / p.uq;
   const size_t half_sm = env_u32("QW_SMEM_KB", 112) * 1024, full_sm = 220 * 1024;
   size_t S = units;
-  auto total = [&](size_t s) {
+  auto total_b = [&](size_t s) {
     return align_up(s * unit_bytes, 128) + fixed + pre_bytes(s) + (2 * s + 2) * 8;
   };
-  while (S > 3 && total(S) > half_sm) --S;
-  while (S > 2 && total(S) > full_sm) --S;
-  if (total(S) > full_sm) return (int)cudaErrorInvalidConfiguration;
+  while (S > 3 && total_b(S) > half_sm) --S;
+  while (S > 2 && total_b(S) > full_sm) --S;
+  if (total_b(S) > full_sm) return (int)cudaErrorInvalidConfiguration;
   p.nslot = (uint32_t)S;
   p.so_off = (uint32_t)align_up(S * unit_bytes, 128);
   p.part_off = p.so_off + (uint32_t)align_up(so_bytes, 16);
@@ -722,22 +755,44 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
   }
   return 0;
 }
+}  // namespace
 
-int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream,
-                bool pdl, unsigned long long* dbg, uint32_t repeat, bool global_clock,
-                uint32_t flags) {
-  const Geometry& G = L.g;
-  const GemvPlan& p = L.plan;
+int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
+  GemvPlan& p = L.plan;
+  if (int e = plan_geometry(p, L.g)) return e;
+  const uint32_t* rp[1] = {host_row_ptr};
+  return plan_ctas(p, L.g, rp, 1, num_sms);
+}
+
+int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_t* const* host_row_ptrs,
+                    uint32_t n, int num_sms) {
+  if (n == 0 || n > kMaxSeg) return (int)cudaErrorInvalidValue;
+  const Geometry& G = layers[0]->g;
+  for (uint32_t l = 1; l < n; ++l) {
+    const Geometry& H = layers[l]->g;
+    if (H.rows != G.rows || H.cols != G.cols || H.n4 != G.n4 || H.n2p != G.n2p || H.group2 != G.group2 ||
+        H.dense_bytes != G.dense_bytes)
+      return (int)cudaErrorInvalidValue;
+  }
+  p = layers[0]->plan;  // geometry part is identical
+  return plan_ctas(p, G, host_row_ptrs, n, num_sms);
+}
+
+int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
+                      float* const* ys, void* stream, bool pdl, uint32_t flags, unsigned long long* dbg,
+                      uint32_t repeat, bool global_clock) {
+  const Geometry& G = layers[0]->g;
   GemvArgs a;
-  a.quads = L.quads;
-  a.sorder = L.sorder;
-  a.row_ptr = L.row_ptr;
-  a.csr = L.csr;
-  a.perm = L.perm16;
+  for (uint32_t l = 0; l < kMaxSeg; ++l) {
+    const DeviceLayer& L = *layers[std::min(l, n - 1)];
+    a.quads[l] = L.quads, a.sorder[l] = L.sorder, a.row_ptr[l] = L.row_ptr;
+    a.csr[l] = L.csr, a.perm[l] = L.perm16, a.s_scale[l] = L.plan.s_scale;
+    a.y[l] = ys[std::min(l, n - 1)];
+  }
+  a.x = x;
   a.g = G;
   a.W = p.warps, a.W2 = p.warps2, a.S = p.nslot;
   a.grid = p.grid, a.nq_max = p.nq_max, a.rb_magic = p.rb_magic, a.rb_one = p.rb_one;
-  a.s_scale = p.s_scale;
   a.so_off = p.so_off, a.part_off = p.part_off, a.csr_off = p.misc_off, a.x_off = p.xg_off, a.win_off = p.win_off, a.pre_off = p.pre_off;
   a.bar_off = p.bar_off;
   a.dbg = dbg;
@@ -746,16 +801,31 @@ int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   a.pre = 1;
   if (const char* e = std::getenv("QW_NO_PRE")) a.pre = std::atoi(e) ? 0u : 1u;
   a.repeat = repeat;
-  std::copy(p.csr_lo, p.csr_lo + p.grid + 1, a.csr_lo);
+  std::copy(p.cta_seg, p.cta_seg + p.grid, a.cta_seg);
+  std::copy(p.cta_q0, p.cta_q0 + p.grid, a.cta_q0);
+  std::copy(p.cta_q1, p.cta_q1 + p.grid, a.cta_q1);
+  std::copy(p.cta_e0, p.cta_e0 + p.grid, a.cta_e0);
+  std::copy(p.cta_e1, p.cta_e1 + p.grid, a.cta_e1);
   const GemvFn fn = pick_kernel(p.kmax, p.uniform_rb, p.xsm);
   const uint32_t threads = (p.warps + 2) * 32;
+  void* params[] = {&a};
+  return (int)launch_ex((const void*)fn, dim3(p.grid), dim3(threads), p.smem, (cudaStream_t)stream, pdl, params);
+}
+
+int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
+                      float* const* ys, void* stream, bool pdl, uint32_t flags) {
+  return launch_gemv_group(p, layers, n, x, ys, stream, pdl, flags, nullptr, 1, false);
+}
+
+int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream,
+                bool pdl, unsigned long long* dbg, uint32_t repeat, bool global_clock,
+                uint32_t flags) {
+  const DeviceLayer* layers[1] = {&L};
   for (uint32_t col = 0; col < batch; ++col) {
-    a.x = x + (size_t)col * G.cols;
-    a.y = y + (size_t)col * G.rows;
-    void* params[] = {&a};
-    cudaError_t err = launch_ex((const void*)fn, dim3(p.grid), dim3(threads), p.smem,
-                                (cudaStream_t)stream, pdl, params);
-    if (err != cudaSuccess) return (int)err;
+    float* ys[1] = {y + (size_t)col * L.g.rows};
+    const int e = launch_gemv_group(L.plan, layers, 1, x + (size_t)col * L.g.cols, ys, stream, pdl, flags,
+                                    dbg, repeat, global_clock);
+    if (e) return e;
   }
   return 0;
 }

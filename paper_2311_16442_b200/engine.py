@@ -187,3 +187,42 @@ class DeviceLayer:
 
 def upload(layer: PackedLayer, device: int = 0) -> DeviceLayer:
     return DeviceLayer(layer, device)
+
+
+class LayerGroup:
+    """Several DeviceLayers of identical geometry that read the same input
+    (q/k/v, gate/up) computed by ONE fused batch-1 launch (qw_group_matvec):
+    the dependency wait and the activation staging are paid once."""
+
+    def __init__(self, layers: list["DeviceLayer"]):
+        self.layers = list(layers)
+        arr = (C.c_void_p * len(layers))(*[d._h.value if hasattr(d._h, "value") else d._h for d in layers])
+        h = C.c_void_p()
+        check(lib().qw_group_create(arr, len(layers), C.byref(h)))
+        self._h = h
+        self.device = layers[0].device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().qw_group_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def matvec(self, x, outs=None, stream=None, pdl: bool = False, x_independent: bool = False):
+        """x: cuda fp32 [cols] (original order); returns one [rows] output per layer."""
+        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous() or x.dim() != 1:
+            raise QWeightError(1, "group matvec: x must be a contiguous 1-D cuda float32 tensor")
+        if x.shape[0] != self.layers[0].cols:
+            raise QWeightError(1, "group matvec: activation length != input channels")
+        if outs is None:
+            outs = [torch.empty(d.rows, dtype=torch.float32, device=x.device) for d in self.layers]
+        ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        flags = (1 if pdl else 0) | (2 if x_independent else 0)
+        check(lib().qw_group_matvec(self._h, C.c_void_p(x.data_ptr()), ptrs,
+                                    C.c_void_p(_stream_handle(stream)), flags))
+        return outs

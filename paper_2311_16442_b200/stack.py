@@ -13,7 +13,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .engine import DeviceLayer, Workspace
+from .engine import DeviceLayer, LayerGroup, Workspace
 
 try:
     import torch
@@ -30,12 +30,19 @@ class _Slot:
 
 class LinearStack:
     def __init__(self, layers: list[DeviceLayer], device: int = 0, batch: int = 1,
-                 pdl: bool = True, depends: list[bool] | None = None):
-        """depends[i]: linear i reads an input produced by linear i-1 (it
-        waits for it); False lets it read its input at once (its input came
-        from the host or an earlier, finished kernel)."""
+                 pdl: bool = True, depends: list[bool] | None = None,
+                 groups: list[list[int]] | None = None):
+        """groups: consecutive index lists of linears that read the same input
+        (q/k/v, gate/up) and run as ONE fused launch (batch 1); default one
+        launch per linear.  depends[i] (per launch): launch i reads an input
+        produced by launch i-1 (it waits for it); False lets it read its input
+        at once (it came from the host or an earlier, finished kernel)."""
         self.device, self.batch, self.pdl = device, batch, pdl
-        self.depends = list(depends) if depends is not None else [True] * len(layers)
+        self.groups = groups if groups is not None else [[i] for i in range(len(layers))]
+        assert [i for g in self.groups for i in g] == list(range(len(layers))), "groups must tile the layers in order"
+        self.depends = list(depends) if depends is not None else [True] * len(self.groups)
+        self.fused = [LayerGroup([layers[i] for i in g]) if len(g) > 1 and batch == 1 else None
+                      for g in self.groups]
         self.dev = torch.device(f"cuda:{device}")
         xo = yo = 0
         self.slots = []
@@ -62,17 +69,26 @@ class LinearStack:
         return self.y[s.y_off:s.y_off + self.batch * s.layer.rows].view(self.batch, s.layer.rows)
 
     # ------------------------------------------------------------ launches
+    def _launch(self, gi, stream=None):
+        g, dep = self.groups[gi], self.depends[gi]
+        if self.fused[gi] is not None:  # one input, one fused launch
+            self.fused[gi].matvec(self.x_of(g[0])[0], outs=[self.y_of(i)[0] for i in g], stream=stream,
+                                  pdl=self.pdl, x_independent=not dep)
+            return
+        for k, i in enumerate(g):
+            self.slots[i].layer.matvec(self.x_of(g[0] if len(g) > 1 else i), out=self.y_of(i),
+                                       workspace=self.ws, stream=stream, pdl=self.pdl,
+                                       x_independent=(not dep) or k > 0)
+
     def launch_step(self, stream=None):
-        for i, s in enumerate(self.slots):
-            s.layer.matvec(self.x_of(i), out=self.y_of(i), workspace=self.ws, stream=stream,
-                           pdl=self.pdl, x_independent=not self.depends[i])
+        for gi in range(len(self.groups)):
+            self._launch(gi, stream)
 
     def launch_subset(self, select, stream=None):
-        """Launch only the linears `select(layer)` accepts (kernel-only timing)."""
-        for i, s in enumerate(self.slots):
-            if select(s.layer):
-                s.layer.matvec(self.x_of(i), out=self.y_of(i), workspace=self.ws, stream=stream,
-                               pdl=self.pdl, x_independent=not self.depends[i])
+        """Launch only the launches whose first layer `select(layer)` accepts (kernel-only timing)."""
+        for gi, g in enumerate(self.groups):
+            if select(self.slots[g[0]].layer):
+                self._launch(gi, stream)
 
     def capture(self):
         """Capture one decode step into a CUDA graph (after a warm run)."""

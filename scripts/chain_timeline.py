@@ -44,7 +44,7 @@ grid = int((a[0, :, 0] > 0).sum())
 a = a[:, :grid, :]
 t0 = a[0, :, 0].min()
 print(f"{rows}x{cols}, {N} kernels, grid {grid}: ns from first entry")
-print("   k   entry0  entry_max   pre_max   dep_min   dep_max    x_max   max_max  prolog_max  unit0_max  cons_max    y_max   y_span")
+print("   k   entry0  entry_max   pre_max   dep_min   dep_max    x_max  gath_max  prolog_max  unit0_max  cons_max    y_max   y_span")
 prev = None
 for i in range(N):
     r = a[i] - t0

@@ -238,3 +238,28 @@ def test_tp_linear_single_rank_nccl(mode):
     tp = TPLinear(layer, 0, 1, mode, device="cuda:0")
     y = tp.forward(torch.from_numpy(x).cuda()).cpu().numpy()
     assert rel_l2(y, oracle.matvec_f64(layer, x)) <= TOL
+
+
+# ---------------------------------------------------------------- group launch
+def test_group_launch_matches_single_layers():
+    """q/k/v-style group: three layers, one input, one fused launch; each
+    output equals (bitwise) the single-layer launch and the f64 oracle."""
+    torch = _torch()
+    layers = [qw.synth_layer(512, 1024, seed=60 + i, outlier_ratio=0.005) for i in range(3)]
+    dls = [qw.DeviceLayer(L) for L in layers]
+    grp = qw.LayerGroup(dls)
+    x = qw.synth_activation(1024, 61)
+    xd = torch.from_numpy(x).cuda()
+    outs = grp.matvec(xd)
+    for L, d, o in zip(layers, dls, outs):
+        y = o.cpu().numpy()
+        assert rel_l2(y, oracle.matvec_f64(L, x)) <= TOL
+        single = d.matvec(xd).cpu().numpy()
+        assert rel_l2(y, single) <= 1e-6
+
+
+def test_group_rejects_mismatched_geometry():
+    a = qw.DeviceLayer(qw.synth_layer(64, 512, seed=1))
+    b = qw.DeviceLayer(qw.synth_layer(64, 1024, seed=2))
+    with pytest.raises(qw.QWeightError):
+        qw.LayerGroup([a, b])
