@@ -154,7 +154,7 @@ struct GemvArgs {
   float s_scale[kMaxSeg];  // 2^-P: keeps (eff - zero2) scale2 2^-P inside fp16
   const float* x;
   Geometry g;
-  uint32_t W, W2, S, grid, nq_max;
+  uint32_t W, W2, T, S, grid, nq_max;  // warps per team, 2-bit warps, teams, ring slots
   uint32_t rb_magic, rb_one;  // row / group2 = rb_one ? row : umulhi(row, rb_magic)
   uint32_t repeat;  // diagnostics: consumers re-run the resident quads this many times
   uint32_t wait_x;  // x is the previous kernel's output: griddepcontrol.wait before reading it
@@ -190,12 +190,14 @@ __device__ __forceinline__ uint32_t win_base(uint32_t l) { return l * 20u + (l >
 // KG groups per lane, NQ quads per ring slot (decoded together for ILP),
 // UNI: group2 % 4 == 0 (a quad never straddles 2-order blocks), XSM: x is
 // staged in shared memory (TMA) before the gather.
-template <int KG, int NQ, bool UNI, bool XSM>
-__global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
+// TM: two teams of consumer warps take alternate units (long quad ranges:
+// group launches, wide layers); then the CTA owns the SM (no PDL co-residency).
+template <int KG, int NQ, bool UNI, bool XSM, bool TM = false>
+__global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 2) ? 1 : 2)
     gemv_kernel(const __grid_constant__ GemvArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const Geometry& G = a.g;
-  const uint32_t W = a.W, S = a.S, dense = G.dense_bytes;
+  const uint32_t W = a.W, T = TM ? a.T : 1u, NC = W * T, S = a.S, dense = G.dense_bytes;
   const uint32_t* s_so = reinterpret_cast<const uint32_t*>(smem + a.so_off);
   float* s_part = reinterpret_cast<float*>(smem + a.part_off);  // [row][warp]
   float* s_csr = reinterpret_cast<float*>(smem + a.csr_off);
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
 
   if (threadIdx.x < S) {
     mbar_init(&s_full[threadIdx.x], 1);
-    mbar_init(&s_empty[threadIdx.x], W);
+    mbar_init(&s_empty[threadIdx.x], W);  // one team consumes a unit
   }
   if (threadIdx.x == 32) mbar_init(s_sobar, 1), mbar_init(s_xbar, 1);
   if (threadIdx.x == 0) stamp(a.dbg, 0);  // entry
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
   __syncthreads();
   pdl_launch_dependents();
 
-  if (warp == W) {
+  if (warp == NC) {
     // ================= producer: the weight stream does not depend on x
     if (lane == 0) {
       const uint32_t so_bytes = nrows ? (row_block(r_end - 1) - rb_first + 1) * G.G2s * 4u : 0u;
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
     return;
   }
 
-  if (warp == W + 1) {
+  if (warp == NC + 1) {
     // ================= outliers: exact fp32 x, CSR order within a row
     const uint32_t e_lo = a.cta_e0[blockIdx.x], e_hi = a.cta_e1[blockIdx.x];
     for (uint32_t t = lane; t <= nrows; t += 32) s_rp[t] = g_row_ptr[r_begin + t] - e_lo;
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
       __syncwarp();
     }
     if (lane == 0) stamp(a.dbg, 6);  // outliers done
-    named_sync(2, (W + 1) * 32);     // meet the consumers for the y store
+    named_sync(2, (NC + 1) * 32);    // meet the consumers for the y store
     return;
   }
 
@@ -322,17 +324,18 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
   // A dead lane (past the last group of its type) decodes a real group with
   // X = 0, so it contributes exact zeros without a branch in the loop.
   const uint32_t W2 = a.W2, W4 = W - W2;
-  const bool two = warp < W2;
+  const uint32_t team = warp / W, wt = warp - team * W;  // warp within its team
+  const bool two = wt < W2;
   uint32_t gk[KG];
   bool lv[KG];
 #pragma unroll
   for (int k = 0; k < KG; ++k) {
     if (two) {
-      const uint32_t g = (warp + (uint32_t)k * W2) * 32u + lane;
+      const uint32_t g = (wt + (uint32_t)k * W2) * 32u + lane;
       lv[k] = g < G.G2;
       gk[k] = lv[k] ? g : G.G2 - 1u;
     } else {
-      const uint32_t b = (warp - W2 + (uint32_t)k * W4) * 32u + lane;
+      const uint32_t b = (wt - W2 + (uint32_t)k * W4) * 32u + lane;
       lv[k] = b < G.T4;
       gk[k] = G.G2 + (lv[k] ? b : G.T4 - 1u);
     }
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
                         pack_h2(ffma2(e23, make_float2(A[i2], A[i3]), make_float2(B[i2], B[i3]))));
     };
     auto pre_at = [&](uint32_t slot, int j, int k) -> uint2& {
-      return s_pre[((slot * NQ + j) * KG + k) * (W * 32) + warp * 32 + lane];
+      return s_pre[((slot * NQ + j) * KG + k) * (W * 32) + wt * 32 + lane];
     };
 
     // ---- asynchronous dequantization: while the previous layer still runs
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
     // resident unit.
     if (TWO) {
       mbar_wait(s_sobar, 0);
-      for (uint32_t u = 0; u < npre; ++u) {
+      for (uint32_t u = team; u < npre; u += T) {
         mbar_wait(&s_full[u], 0);
         const uint8_t* sb = smem + (size_t)u * NQ * dense;
 #pragma unroll
@@ -504,8 +507,10 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
     }
 
     for (uint32_t rep = 0; rep < reps; ++rep) {
-      uint32_t slot = 0, phase = 0, wrow = 0, wrow0 = 0;
-      for (uint32_t u = 0; u < nunit; ++u) {
+      uint32_t slot = team, phase = 0, wrow = 0, wn = 0;
+      uint32_t wbase[kWinRows / (4 * NQ)];  // CTA-relative first row of each unit in the window
+      while (slot >= S) slot -= S, phase ^= 1u;
+      for (uint32_t u = team; u < nunit; u += T) {
         mbar_wait(&s_full[slot], phase);
         const uint8_t* sb = smem + (size_t)slot * NQ * dense;
         float acc[NQ][4];
@@ -574,8 +579,9 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
         for (int j = 0; j < NQ; ++j)
           *reinterpret_cast<float4*>(win + win_base(lane) + wrow + 4 * j) =
               make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
+        wbase[wn++] = u * NQ * kRowsPerQuad;
         wrow += 4 * NQ;
-        if (wrow == kWinRows || u + 1 == nunit) {  // window full: rows over lanes, lane order
+        if (wrow == kWinRows || u + T >= nunit) {  // window full: rows over lanes, lane order
           __syncwarp();
           const uint32_t row = lane & 15u, src0 = lane & 16u;
           float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
@@ -589,12 +595,12 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
           float sum = (s0 + s1) + (s2 + s3);
           const float other = __shfl_xor_sync(0xFFFFFFFFu, sum, 16);
           sum = src0 ? other + sum : sum + other;  // lanes 0-15 first, then 16-31
-          const uint32_t r = wrow0 + row;
-          if (src0 == 0 && row < wrow && r < nrows) s_part[r * W + warp] = sum * yscale;
+          const uint32_t r = wbase[min(row / (4 * NQ), (uint32_t)(kWinRows / (4 * NQ)) - 1u)] + row % (4 * NQ);
+          if (src0 == 0 && row < wrow && r < nrows) s_part[r * W + wt] = sum * yscale;
           __syncwarp();
-          wrow0 += wrow, wrow = 0;
+          wrow = 0, wn = 0;
         }
-        if (++slot == S) slot = 0, phase ^= 1u;
+        for (slot += T; slot >= S;) slot -= S, phase ^= 1u;
       }
     }
   };
@@ -603,9 +609,9 @@ __global__ void __launch_bounds__(KG <= 2 ? 320 : 544, KG <= 2 ? 2 : 1)
   else
     run(std::false_type{});
   if (threadIdx.x == 0) stamp(a.dbg, 4);  // consumers done
-  named_sync(2, (W + 1) * 32);           // partials and outlier sums complete
+  named_sync(2, (NC + 1) * 32);          // partials and outlier sums complete
   // the dense sum first (fixed warp order), then the outliers, as row_fma (engine.cpp:111-122)
-  for (uint32_t t = threadIdx.x; t < nrows; t += W * 32) {
+  for (uint32_t t = threadIdx.x; t < nrows; t += NC * 32) {
     const float* p = s_part + t * W;
     float s = p[0];
     for (uint32_t w2 = 1; w2 < W; ++w2) s += p[w2];
@@ -630,6 +636,9 @@ GemvFn pick2(uint32_t kg) {
     case 3: return gemv_kernel<3, 1, UNI, XSM>;
     default: return gemv_kernel<4, 1, UNI, XSM>;
   }
+}
+GemvFn pick_teams(uint32_t kg) {
+  return kg == 1 ? gemv_kernel<1, 2, true, true, true> : gemv_kernel<2, 2, true, true, true>;
 }
 GemvFn pick_kernel(uint32_t kg, bool uni, bool xsm) {
   return uni ? (xsm ? pick2<true, true>(kg) : pick2<true, false>(kg))
@@ -707,10 +716,11 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
     }
   }
   const size_t so_bytes = (size_t)so_rows_max * G.G2s * 4;
-  const size_t part_bytes = (size_t)p.nq_max * p.warps * 16;
+  const size_t part_bytes = (size_t)p.nq_max * p.warps * 16;  // [row][warp of a team]
   const size_t misc_bytes = (size_t)p.nq_max * 4 * 4 + ((size_t)p.nq_max * 4 + 4) * 4 + 256 * 4 + 64 * 4;
   const size_t x_bytes = p.xsm ? align_up((size_t)G.cols * 4, 16) : 0;
-  const size_t win_bytes = (size_t)p.warps * kWinWords * 4;
+  const uint32_t tmax = (p.kmax <= 2 && p.uniform_rb && p.xsm && p.uq == 2) ? 2u : 1u;
+  const size_t win_bytes = (size_t)p.warps * tmax * kWinWords * 4;
   const size_t fixed = align_up(so_bytes, 16) + part_bytes + align_up(misc_bytes, 16) + x_bytes +
                        win_bytes + 64;
   // precomputed 1st-order scales: one uint2 per (slot, quad, k, lane)
@@ -719,7 +729,9 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   // layer's CTA fits beside it under PDL), else as many slots as fit
   const size_t unit_bytes = (size_t)p.uq * G.dense_bytes;
   const size_t units = (p.nq_max + p.uq - 1) / p.uq;
-  const size_t half_sm = env_u32("QW_SMEM_KB", 112) * 1024, full_sm = 220 * 1024;
+  // long ranges (group launches, big layers): two teams, the whole SM
+  p.teams = (p.nq_max >= env_u32("QW_TEAMS_MIN_NQ", 12) && p.kmax <= 2 && p.uniform_rb && p.xsm && p.uq == 2) ? 2 : 1;
+  const size_t half_sm = (p.teams == 2 ? 200 : env_u32("QW_SMEM_KB", 112)) * 1024, full_sm = 220 * 1024;
   size_t S = units;
   auto total_b = [&](size_t s) {
     return align_up(s * unit_bytes, 128) + fixed + pre_bytes(s) + (2 * s + 2) * 8;
@@ -749,6 +761,11 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
     for (bool xsm : {false, true}) {
       cudaError_t err = cudaFuncSetAttribute(xsm ? gemv_kernel<1, 2, true, true> : gemv_kernel<1, 2, true, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+      if (err != cudaSuccess) return (int)err;
+    }
+    for (uint32_t k : {1u, 2u}) {
+      cudaError_t err = cudaFuncSetAttribute(pick_teams(k), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(227 * 1024));
       if (err != cudaSuccess) return (int)err;
     }
     attr_set = true;
@@ -791,7 +808,7 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   }
   a.x = x;
   a.g = G;
-  a.W = p.warps, a.W2 = p.warps2, a.S = p.nslot;
+  a.W = p.warps, a.W2 = p.warps2, a.T = p.teams, a.S = p.nslot;
   a.grid = p.grid, a.nq_max = p.nq_max, a.rb_magic = p.rb_magic, a.rb_one = p.rb_one;
   a.so_off = p.so_off, a.part_off = p.part_off, a.csr_off = p.misc_off, a.x_off = p.xg_off, a.win_off = p.win_off, a.pre_off = p.pre_off;
   a.bar_off = p.bar_off;
@@ -806,8 +823,8 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   std::copy(p.cta_q1, p.cta_q1 + p.grid, a.cta_q1);
   std::copy(p.cta_e0, p.cta_e0 + p.grid, a.cta_e0);
   std::copy(p.cta_e1, p.cta_e1 + p.grid, a.cta_e1);
-  const GemvFn fn = pick_kernel(p.kmax, p.uniform_rb, p.xsm);
-  const uint32_t threads = (p.warps + 2) * 32;
+  const GemvFn fn = p.teams == 2 ? pick_teams(p.kmax) : pick_kernel(p.kmax, p.uniform_rb, p.xsm);
+  const uint32_t threads = (p.warps * p.teams + 2) * 32;
   void* params[] = {&a};
   return (int)launch_ex((const void*)fn, dim3(p.grid), dim3(threads), p.smem, (cudaStream_t)stream, pdl, params);
 }
