@@ -221,6 +221,9 @@ int qw_debug_timeline(const qw_layer* layer, const float* x, float* y,
                       unsigned long long* stamps, uint32_t repeat, uint32_t flags,
                       void* stream);
 int qw_debug_timeline_events(void);
+/* Same for a group launch (flags as qw_debug_timeline). */
+int qw_debug_group_timeline(const qw_group* group, const float* x, float* const* ys,
+                            unsigned long long* stamps, uint32_t flags, void* stream);
 /* Diagnostics: one batched (K4) matvec stamping %globaltimer per CTA into
  * stamps [grid][8]: 0 setup, 1 first A tile, 2 last A tile, 3 accumulator
  * ready, 4 epilogue staged, 5 split partials parked, 6 y stored. */

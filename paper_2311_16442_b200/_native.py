@@ -102,6 +102,8 @@ _SIGS = {
     "qw_debug_timeline": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
                                       C.c_uint32, C.c_void_p]),
     "qw_debug_timeline_events": (C.c_int, []),
+    "qw_debug_group_timeline": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p,
+                                          C.c_uint32, C.c_void_p]),
     "qw_debug_gemm_timeline": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
                                          C.c_void_p]),
     "qw_launches_per_matvec": (C.c_int, [C.c_void_p, C.c_uint32]),

@@ -754,6 +754,16 @@ int qw_group_matvec(const qw_group* g, const float* x, float* const* ys, void* s
   return e ? cuda_fail((cudaError_t)e, "group launch") : QW_OK;
 }
 
+int qw_debug_group_timeline(const qw_group* g, const float* x, float* const* ys, unsigned long long* stamps,
+                            uint32_t flags, void* stream) {
+  if (!g || !x || !ys || !stamps) return fail(QW_ERR_ARG, "timeline: null argument");
+  cudaSetDevice(g->device);
+  const int e = qwdev::launch_gemv_group(g->plan, g->layers.data(), (uint32_t)g->layers.size(), x, ys, stream,
+                                         flags & 1u, (flags & 4u) ? qwdev::kXIndependent : 0u, stamps, 1,
+                                         (flags & 2u) != 0);
+  return e ? cuda_fail((cudaError_t)e, "group launch") : QW_OK;
+}
+
 int qw_debug_gemm_timeline(const qw_layer* L, const float* x, uint32_t batch, float* y,
                            unsigned long long* stamps, void* stream) {
   if (!L || !x || !y || !stamps) return fail(QW_ERR_ARG, "timeline: null argument");

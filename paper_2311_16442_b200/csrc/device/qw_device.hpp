@@ -106,6 +106,9 @@ int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_
                     uint32_t n, int num_sms);
 int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
                       float* const* ys, void* stream, bool pdl, uint32_t flags);
+int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
+                      float* const* ys, void* stream, bool pdl, uint32_t flags, unsigned long long* dbg,
+                      uint32_t repeat, bool global_clock);
 // y[col] = W_q x[col] for col < batch: one fused kernel per column.
 constexpr uint32_t kTimelineEvents = 12;  // entry, copies issued, prologue, first quad, consumers, y, csr
 // flags: kXIndependent = x was not written by the preceding kernel on the

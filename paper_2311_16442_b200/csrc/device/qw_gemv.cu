@@ -295,13 +295,20 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     };
     if (n) fetch(0);
     __syncwarp();
-    if (n && a.wait_x) pdl_wait();  // x is the previous kernel's output
+    // x: the shared-memory copy once it lands (XSM), else global after the
+    // dependency wait (x is the previous kernel's output)
+    if (n) {
+      if (XSM)
+        mbar_wait(s_xbar, 0);
+      else if (a.wait_x)
+        pdl_wait();
+    }
     for (uint32_t c0 = 0; c0 < n; c0 += 32u * kPer) {
       const uint32_t c1 = min(c0 + 32u * kPer, n);
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
         const uint32_t e = c0 + lane + 32u * j;
-        if (e < c1) s_prod[e - c0] = half_bits_to_float(ent[j] >> 16) * __ldg(a.x + src[j]);
+        if (e < c1) s_prod[e - c0] = half_bits_to_float(ent[j] >> 16) * (XSM ? s_x[src[j]] : __ldg(a.x + src[j]));
       }
       __syncwarp();
       if (c1 < n) fetch(c1);
