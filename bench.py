@@ -245,7 +245,7 @@ def run_ours(args):
         groups += [[b, b + 1, b + 2], [b + 3], [b + 4, b + 5], [b + 6]] if not args.ungrouped else \
                   [[b + i] for i in range(7)]
     stack = LinearStack([d for _, d in per_layer], device=local, batch=1, pdl=not args.no_pdl,
-                        groups=groups)
+                        groups=groups, prefetch=args.prefetch)
     # q/k/v read one activation, gate/up another (the grouped launches' shared inputs)
     src = {0: 0, 1: 0, 2: 0, 3: 3, 4: 4, 5: 4, 6: 6}
     x_all = np.concatenate([qw.synth_activation(base[i].cfg.cols, 1000 * l + src[i])
@@ -359,7 +359,9 @@ def run_ours(args):
                        "batch": 1, "bytes_per_step": step_bytes,
                        "l2": "inputs larger than L2 (distinct HBM copy per GEMV)",
                        "launch": "CUDA graph, programmatic dependent launch" if not args.no_pdl
-                                 else "CUDA graph"},
+                                 else "CUDA graph",
+                       "prefetch": "none" if not args.prefetch else
+                                   "each launch streams the next launch's weights HBM->L2 (read once per step)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved_q, 2), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved_q / hbm_peak, 4),
                          "traffic": traffic, "peak_kind": peak_kind,
@@ -389,6 +391,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=32, help="decoder layers per step")
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--prefetch", action="store_true", help="L2 prefetch of the next launch's weights")
     ap.add_argument("--ungrouped", action="store_true", help="one launch per linear (no q/k/v, gate/up fusion)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU sample")

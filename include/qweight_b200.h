@@ -189,6 +189,13 @@ int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out);
 int qw_group_free(qw_group* group);
 int qw_group_matvec(const qw_group* group, const float* x, float* const* ys, void* stream,
                     uint32_t flags);
+/* Decode chains: while a launch of `layer` (or `group`) runs, its CTAs also
+ * stream the packed weights of `next` (the layers of the launch that follows
+ * on the stream) from HBM into L2, so HBM keeps streaming while the SMs finish
+ * this launch and the next one reads L2.  A hint: results never depend on it.
+ * n = 0 clears.  The next layers must outlive the setting. */
+int qw_layer_set_prefetch(qw_layer* layer, const qw_layer* const* next, uint32_t n);
+int qw_group_set_prefetch(qw_group* group, const qw_layer* const* next, uint32_t n);
 /* Host-buffer, synchronous, checked: length and finiteness as the reference
  * (engine.cpp:124-132).  x_len must equal batch * cols. */
 int qw_matvec_host(const qw_layer* layer, const float* x, uint64_t x_len,

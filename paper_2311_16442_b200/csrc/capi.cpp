@@ -514,7 +514,7 @@ int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
     repack(L, H->dev.g, quads, sorder, csr);
     std::vector<uint16_t> perm16(L.plan.perm.size());
     for (size_t i = 0; i < perm16.size(); ++i)
-      perm16[i] = L.plan.perm[i] == qwb::kPad ? 0 : (uint16_t)L.plan.perm[i];
+      perm16[i] = L.plan.perm[i] == qwb::kPad ? (uint16_t)L.cfg.cols : (uint16_t)L.plan.perm[i];  // pads: x[cols] = 0 slot
     H->host_row_ptr = L.csr.row_ptr;
     if (H->host_row_ptr.empty()) H->host_row_ptr.assign((size_t)L.cfg.rows + 1, 0u);
     if (int pe = qwdev::plan_gemv(H->dev, H->num_sms, H->host_row_ptr.data())) {
@@ -752,6 +752,40 @@ int qw_group_matvec(const qw_group* g, const float* x, float* const* ys, void* s
                                          (flags & QW_LAUNCH_PDL) != 0,
                                          (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u);
   return e ? cuda_fail((cudaError_t)e, "group launch") : QW_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int set_prefetch(qwdev::GemvPlan& p, int device, const qw_layer* const* next, uint32_t n) {
+  if (n && !next) return fail(QW_ERR_ARG, "prefetch: null layer list");
+  if (2 * n > qwdev::GemvPlan::kMaxPf) return fail(QW_ERR_UNSUPPORTED, "prefetch: at most 4 next layers");
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!next[i]) return fail(QW_ERR_ARG, "prefetch: null layer");
+    if (next[i]->device != device) return fail(QW_ERR_ARG, "prefetch: layer on another device");
+  }
+  p.pf_n = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const qwdev::DeviceLayer& d = next[i]->dev;
+    p.pf_ptr[p.pf_n] = d.quads;
+    p.pf_bytes[p.pf_n++] = d.g.quads * d.g.dense_bytes;
+    p.pf_ptr[p.pf_n] = reinterpret_cast<const uint8_t*>(d.sorder);
+    p.pf_bytes[p.pf_n++] = d.g.row_blocks * d.g.G2s * 4u;
+  }
+  return QW_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int qw_layer_set_prefetch(qw_layer* L, const qw_layer* const* next, uint32_t n) {
+  if (!L) return fail(QW_ERR_ARG, "prefetch: null layer");
+  return set_prefetch(L->dev.plan, L->device, next, n);
+}
+
+int qw_group_set_prefetch(qw_group* g, const qw_layer* const* next, uint32_t n) {
+  if (!g) return fail(QW_ERR_ARG, "prefetch: null group");
+  return set_prefetch(g->plan, g->device, next, n);
 }
 
 int qw_debug_group_timeline(const qw_group* g, const float* x, float* const* ys, unsigned long long* stamps,

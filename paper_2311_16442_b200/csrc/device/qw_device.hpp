@@ -44,11 +44,19 @@ constexpr uint32_t kMaxGrid = 448;
 struct GemvPlan {
   uint32_t grid = 0;                   // CTAs (persistent, contiguous quad ranges)
   uint32_t warps = 0, warps2 = 0, teams = 1, kmax = 0;  // consumer warps, 32-group chunks per warp
+  bool wide = false;  // W > 8 warps of KG = 2 (wide layers): one CTA per SM, the 576-thread kernel
   uint32_t nslot = 0, uq = 2, win = 0;  // slots, quads per slot, quads per reduction window
   uint32_t nchunks = 0, nq_max = 0, uniform_rb = 0, xsm = 0, rb_magic = 0, rb_one = 0;
   float s_scale = 1.0f;  // 2^-P applied to 2-bit s1 so 15 * max scale2 * 2^-P fits fp16
   uint32_t so_off = 0, part_off = 0, xg_off = 0, misc_off = 0, win_off = 0, pre_off = 0, bar_off = 0;  // smem layout
   uint32_t smem = 0;
+  // decode chains: the next launch's packed weights (quad records, 2-order
+  // rows), streamed into L2 by this launch's CTAs (one slice each) so HBM
+  // keeps streaming while the SMs are still busy with this launch
+  static constexpr uint32_t kMaxPf = 8;
+  const uint8_t* pf_ptr[kMaxPf] = {};
+  uint32_t pf_bytes[kMaxPf] = {};
+  uint32_t pf_n = 0;
   // per CTA: layer (segment) of a group launch, quad range, CSR entry range
   uint8_t cta_seg[kMaxGrid] = {};
   uint32_t cta_q0[kMaxGrid] = {}, cta_q1[kMaxGrid] = {}, cta_e0[kMaxGrid] = {}, cta_e1[kMaxGrid] = {};
@@ -84,7 +92,7 @@ struct DeviceLayer {
   uint8_t* quads = nullptr;      // quads * dense_bytes
   uint32_t* sorder = nullptr;    // row_blocks * G2s
   uint32_t* perm = nullptr;      // padded_cols (0xFFFFFFFF = pad)
-  uint16_t* perm16 = nullptr;    // padded_cols, original channel (pads 0; known by position)
+  uint16_t* perm16 = nullptr;    // padded_cols, original channel (pads: cols, a zero slot of the staged x)
   uint32_t* row_ptr = nullptr;   // rows + 1
   uint32_t* csr = nullptr;       // nnz (col | fp16 << 16)
 };

@@ -66,6 +66,14 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
 __device__ __forceinline__ float pow2f(int e) {  // 2^e for -126 <= e <= 127
   return __uint_as_float((uint32_t)(e + 127) << 23);
 }
@@ -159,7 +167,10 @@ struct GemvArgs {
   uint32_t repeat;  // diagnostics: consumers re-run the resident quads this many times
   uint32_t wait_x;  // x is the previous kernel's output: griddepcontrol.wait before reading it
   uint32_t pre;     // precompute 1st-order scales of resident units before x
+  uint32_t x_first; // stage x before the scale precompute (no predecessor overlap)
   uint32_t so_off, part_off, csr_off, x_off, win_off, pre_off, bar_off;
+  const uint8_t* pf_ptr[GemvPlan::kMaxPf];  // next launch's weights -> L2 (a slice per CTA)
+  uint32_t pf_bytes[GemvPlan::kMaxPf], pf_n, pf_late;
   unsigned long long* dbg;  // optional timeline: kTimelineEvents stamps per CTA
   uint32_t dbg_global;      // stamps from %globaltimer (ns) instead of clock64
   uint8_t cta_seg[kMaxGrid];
@@ -179,13 +190,14 @@ __device__ __forceinline__ void stamp_impl(const GemvArgs& a, uint32_t ev) {
     if (DBG) stamp_impl(a, EV); \
   } while (0)
 
-// Per-warp reduction window of 16 rows: lane l stores its partial of row r at
-// win[wbase(l) + r], wbase(l) = l * 20 (+16 for l >= 16): 16-byte stores and
-// the transposed reads are both bank-conflict free.  When the window is full,
-// lane l sums row l & 15 over source lanes 16 (l >> 4) .. +15 in lane order,
-// one shuffle joins the halves (fixed order: deterministic).
-constexpr uint32_t kWinRows = 16, kWinWords = 656;
-__device__ __forceinline__ uint32_t win_base(uint32_t l) { return l * 20u + (l >= 16u ? 16u : 0u); }
+// Per-warp reduction window of 16 rows: lane l stores its partials of rows
+// r..r+3 at win[wbase(l) + r] (16-byte stores, conflict-free per quarter
+// warp), wbase(l) = 20 l + 16 (l >> 3).  When the window is full, lane l sums
+// the row pair 2 (l & 7), +1 over source lanes 8 (l >> 3) .. +7 (8-byte reads:
+// the two source groups of a half-warp sit 16 banks apart), two shuffles join
+// the four source groups (a fixed tree: deterministic).
+constexpr uint32_t kWinRows = 16, kWinWords = 688;
+__device__ __forceinline__ uint32_t win_base(uint32_t l) { return l * 20u + (l >> 3) * 16u; }
 
 // KG groups per lane, NQ quads per ring slot (decoded together for ILP),
 // UNI: group2 % 4 == 0 (a quad never straddles 2-order blocks), XSM: x is
@@ -233,7 +245,8 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     mbar_init(&s_full[threadIdx.x], 1);
     mbar_init(&s_empty[threadIdx.x], W);  // one team consumes a unit
   }
-  if (threadIdx.x == 32) mbar_init(s_sobar, 1), mbar_init(s_xbar, 1);
+  if (threadIdx.x == 32) mbar_init(s_sobar, 1), mbar_init(s_xbar, NC);
+  if (XSM && threadIdx.x == 64) s_x[G.cols] = 0.0f;  // pads gather this zero (perm16 = cols)
   if (threadIdx.x == 0) stamp(a.dbg, 0);  // entry
   mbar_fence_init();
   __syncthreads();
@@ -250,28 +263,39 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
         mbar_arrive(s_sobar);
       }
       const uint8_t* src = g_quads + (size_t)q0 * dense;
-      const uint32_t npre = min(nunit, S);
+      // L2 prefetch of this CTA's slice of the next launch's weights, issued
+      // in step with the own units so the ring refills never queue behind it
+      uint32_t pf_r = 0, pf_pos = 0, pf_end = 0;
+      uint64_t pf_total = 0, pf_done = 0;
+      for (uint32_t r = 0; r < a.pf_n; ++r) pf_total += a.pf_bytes[r] / a.grid / 16u * 16u;
+      auto pf_region = [&](uint32_t r) {  // this CTA's 16-byte aligned slice of region r
+        const uint32_t per = a.pf_bytes[r] / a.grid / 16u * 16u;
+        pf_pos = per * blockIdx.x;
+        pf_end = blockIdx.x + 1 == a.grid ? a.pf_bytes[r] / 16u * 16u : pf_pos + per;
+      };
+      if (a.pf_n) pf_region(0);
+      auto prefetch_upto = [&](uint64_t target) {
+        while (pf_done < target && pf_r < a.pf_n) {
+          if (pf_pos >= pf_end) {
+            if (++pf_r < a.pf_n) pf_region(pf_r);
+            continue;
+          }
+          const uint32_t n = min(pf_end - pf_pos, 32768u);
+          bulk_prefetch_l2(a.pf_ptr[pf_r] + pf_pos, n);
+          pf_pos += n, pf_done += n;
+        }
+      };
       uint32_t slot = 0, phase = 0;
       for (uint32_t u = 0; u < nunit; ++u) {
-        if (u == npre && XSM) {  // resident units queued: now the activation (previous kernel's output)
-          if (a.wait_x) pdl_wait();
-          stamp(a.dbg, 1);  // dependency resolved
-          mbar_expect_tx(s_xbar, G.cols * 4u);
-          bulk_load_nohint(s_x, a.x, G.cols * 4u, s_xbar);
-        }
         const uint32_t bytes = min((uint32_t)NQ, nq - NQ * u) * dense;
         if (u >= S) mbar_wait(&s_empty[slot], phase ^ 1u);
         mbar_expect_tx(&s_full[slot], bytes);
         bulk_load_nohint(smem + (size_t)slot * NQ * dense, src, bytes, &s_full[slot]);
         src += bytes;
         if (++slot == S) slot = 0, phase ^= 1u;
+        if (!a.pf_late) prefetch_upto(pf_total * (u + 1) / nunit);
       }
-      if (npre == nunit && XSM) {
-        if (a.wait_x) pdl_wait();
-        stamp(a.dbg, 1);  // dependency resolved
-        mbar_expect_tx(s_xbar, G.cols * 4u);
-        bulk_load_nohint(s_x, a.x, G.cols * 4u, s_xbar);
-      }
+      prefetch_upto(~0ull);
     }
     return;
   }
@@ -419,6 +443,41 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
       return s_pre[((slot * NQ + j) * KG + k) * (W * 32) + wt * 32 + lane];
     };
 
+    // ---- x (the previous kernel's output) -> shared memory: coalesced loads
+    // spread over every consumer thread (not queued behind the weight TMAs).
+    // x_first (the CTA starts after its predecessor finished, e.g. it cannot
+    // co-reside with it): the loads are issued first and land under the
+    // scale decode below; else after it (the decode overlaps the predecessor).
+    const uint32_t tid = threadIdx.x, nth = NC * 32u;
+    const bool xvec = (((uintptr_t)a.x) & 15u) == 0 && (G.cols & 3u) == 0;
+    const float4* gx = reinterpret_cast<const float4*>(a.x);
+    float4* sx4 = reinterpret_cast<float4*>(s_x);
+    const uint32_t n4 = G.cols >> 2;
+    constexpr int kXr = 4;
+    float4 xr[kXr];
+    auto x_issue = [&]() {
+      if (a.wait_x) pdl_wait();
+      if (threadIdx.x == 0) stamp(a.dbg, 1);  // dependency resolved
+      if (xvec) {
+#pragma unroll
+        for (int j = 0; j < kXr; ++j)
+          if (tid + j * nth < n4) xr[j] = __ldg(gx + tid + j * nth);
+      }
+    };
+    auto x_store = [&]() {
+      if (xvec) {
+#pragma unroll
+        for (int j = 0; j < kXr; ++j)
+          if (tid + j * nth < n4) sx4[tid + j * nth] = xr[j];
+        for (uint32_t i = tid + kXr * nth; i < n4; i += nth) sx4[i] = __ldg(gx + i);
+      } else {
+        for (uint32_t i = tid; i < G.cols; i += nth) s_x[i] = __ldg(a.x + i);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_xbar);
+    };
+    if (XSM && a.x_first) x_issue();
+
     // ---- asynchronous dequantization: while the previous layer still runs
     // (its output x is not needed yet), decode the 1st-order scales of every
     // resident unit.
@@ -450,6 +509,8 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     if (threadIdx.x == 0) stamp(a.dbg, 8);  // x-independent work done
     const float* xs;
     if (XSM) {
+      if (!a.x_first) x_issue();
+      x_store();
       mbar_wait(s_xbar, 0);
       if (threadIdx.x == 0) stamp(a.dbg, 7);  // x landed
       xs = s_x;
@@ -465,22 +526,28 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
       const uint32_t s0 = 16u * gk[k];
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj) {
-        const uint32_t c = (pw[k][jj >> 1] >> (16 * (jj & 1))) & 0xFFFFu;
-        float v = XSM ? xs[c] : __ldg(xs + c);
-        if (TWO && s0 + jj >= n2 && s0 + jj < G.n2p) v = 0.0f;  // pads (apply_permutation)
-        if (!lv[k]) v = 0.0f;
+        uint32_t c = (pw[k][jj >> 1] >> (16 * (jj & 1))) & 0xFFFFu;
+        float v;
+        if (XSM) {
+          v = xs[c];  // pads read the zero slot xs[cols]
+        } else {
+          v = __ldg(xs + min(c, G.cols - 1u));
+          if (TWO && s0 + jj >= n2 && s0 + jj < G.n2p) v = 0.0f;  // pads (apply_permutation)
+        }
         xv[k][jj] = v;
         mx = fmaxf(mx, fabsf(v));
       }
     }
-    // one scale per warp (a shuffle reduction, no CTA barrier): the row sums
-    // of a warp's lanes then share it and it is undone once per row
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    // one scale per warp (a single-instruction integer max over the lanes: |x|
+    // bits order like the values), no CTA barrier: the row sums of a warp's
+    // lanes share it and it is undone once per row
+    const uint32_t mxb = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(mx));
     if (threadIdx.x == 0) stamp(a.dbg, 9);  // gathered
-    const int eb = (int)((__float_as_uint(mx) >> 23) & 0xFFu);
+    const int eb = (int)(mxb >> 23);
     const int sh = (eb == 0 ? -126 : eb - 127) - 10;  // floor(log2 max) - 10
-    // x' 2^-b as two normal power-of-two factors (any finite x), b = bit position
+    // x' 2^-b as one power-of-two factor, or two when 2^(-sh-b) leaves the
+    // normal range (extreme x); warp-uniform
+    const bool split = (-sh > 127) || (-sh - (TWO ? 6 : 12) < -126);
     float f1[4], f2[4];
 #pragma unroll
     for (int bi = 0; bi < 4; ++bi) {
@@ -492,18 +559,22 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
 #pragma unroll
     for (int k = 0; k < KG; ++k) {
       const uint32_t g = gk[k];
-      float sx = 0.0f;
+      // a dead lane (past its type's last group) decodes a real group with X = 0
+      const float live = lv[k] ? 1.0f : 0.0f;
+      float sb[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // sum of x' 2^-b per bit position
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj) {
         const int bi = TWO ? (jj & 3) : (jj & 1);
-        const int b = TWO ? 2 * bi : 4 * bi;
-        const __half hh = __float2half_rn(xv[k][jj] * f1[bi] * f2[bi]);
-        X[k][jj] = __half2half2(hh);
-        sx += __half2float(hh) * pow2f(b - 24);
+        float xf = xv[k][jj] * (f1[bi] * live);
+        if (split) xf *= f2[bi];
+        X[k][jj] = __float2half2_rn(xf);
+        sb[bi] += xf;
       }
+      const float sx = TWO ? (sb[0] + sb[1] * 4.0f) + (sb[2] * 16.0f + sb[3] * 64.0f)
+                           : sb[0] + sb[1] * 16.0f;  // sum x' = sum_b 2^b (sum x' 2^-b)
       // zero point: z lands at 2^(2 sub - 24) (2-bit) or 2^-24 (4-bit): z_h nsxh = -z sum x'
       const int zp = TWO ? 2 * (int)(g - 3u * (g / 3u)) : 0;
-      nsxh[k] = __float2half2_rn(-sx * pow2f(24 - zp));
+      nsxh[k] = __float2half2_rn(-sx * pow2f(-zp));
     }
     // every accumulated term is in units of 2^(sh + 24) (and 2^P for 2-bit s1)
     const float yscale = pow2f(max(-126, min(127, sh + 24))) * (TWO ? 1.0f / s_scale : 1.0f);
@@ -514,8 +585,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     }
 
     for (uint32_t rep = 0; rep < reps; ++rep) {
-      uint32_t slot = team, phase = 0, wrow = 0, wn = 0;
-      uint32_t wbase[kWinRows / (4 * NQ)];  // CTA-relative first row of each unit in the window
+      uint32_t slot = team, phase = 0, wrow = 0, ufirst = 0;
       while (slot >= S) slot -= S, phase ^= 1u;
       for (uint32_t u = team; u < nunit; u += T) {
         mbar_wait(&s_full[slot], phase);
@@ -586,26 +656,25 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
         for (int j = 0; j < NQ; ++j)
           *reinterpret_cast<float4*>(win + win_base(lane) + wrow + 4 * j) =
               make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
-        wbase[wn++] = u * NQ * kRowsPerQuad;
+        if (wrow == 0) ufirst = u;
         wrow += 4 * NQ;
-        if (wrow == kWinRows || u + T >= nunit) {  // window full: rows over lanes, lane order
+        if (wrow == kWinRows || u + T >= nunit) {  // window full: row pairs over lanes
           __syncwarp();
-          const uint32_t row = lane & 15u, src0 = lane & 16u;
-          float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+          const uint32_t rp = 2u * (lane & 7u);  // rows rp, rp + 1 of the window
+          const float* src = win + win_base(lane & 24u) + rp;
+          float2 sum = *reinterpret_cast<const float2*>(src);
 #pragma unroll
-          for (uint32_t l = 0; l < 16; l += 4) {
-            s0 += win[win_base(src0 + l + 0) + row];
-            s1 += win[win_base(src0 + l + 1) + row];
-            s2 += win[win_base(src0 + l + 2) + row];
-            s3 += win[win_base(src0 + l + 3) + row];
+          for (uint32_t l = 1; l < 8; ++l) sum = fadd2(sum, *reinterpret_cast<const float2*>(src + 20u * l));
+          sum = fadd2(sum, make_float2(__shfl_xor_sync(0xFFFFFFFFu, sum.x, 8), __shfl_xor_sync(0xFFFFFFFFu, sum.y, 8)));
+          sum = fadd2(sum, make_float2(__shfl_xor_sync(0xFFFFFFFFu, sum.x, 16), __shfl_xor_sync(0xFFFFFFFFu, sum.y, 16)));
+          // window row rp of unit ufirst + (rp / 4 NQ) T (a team's units are T apart)
+          const uint32_t r = (ufirst + (rp / (4 * NQ)) * T) * NQ * kRowsPerQuad + rp % (4 * NQ);
+          if (lane < 8 && rp < wrow) {
+            if (r < nrows) s_part[r * W + wt] = sum.x * yscale;
+            if (r + 1 < nrows) s_part[(r + 1) * W + wt] = sum.y * yscale;
           }
-          float sum = (s0 + s1) + (s2 + s3);
-          const float other = __shfl_xor_sync(0xFFFFFFFFu, sum, 16);
-          sum = src0 ? other + sum : sum + other;  // lanes 0-15 first, then 16-31
-          const uint32_t r = wbase[min(row / (4 * NQ), (uint32_t)(kWinRows / (4 * NQ)) - 1u)] + row % (4 * NQ);
-          if (src0 == 0 && row < wrow && r < nrows) s_part[r * W + wt] = sum * yscale;
           __syncwarp();
-          wrow = 0, wn = 0;
+          wrow = 0;
         }
         for (slot += T; slot >= S;) slot -= S, phase ^= 1u;
       }
@@ -688,12 +757,16 @@ int plan_geometry(GemvPlan& p, const Geometry& G) {
   p.kmax = 1;
   while (p.kmax < 4 && warps_for(p.kmax) > (p.kmax <= 2 ? 8u : 15u)) ++p.kmax;
   if (warps_for(p.kmax) > 15) return (int)cudaErrorInvalidConfiguration;
+  p.uniform_rb = (G.group2 % kRowsPerQuad) == 0;
+  p.xsm = G.cols <= 12288;
+  // wide layers (down_proj): KG = 2 over up to 16 warps in one CTA per SM
+  // rather than KG >= 3 (register spills) in two
+  p.wide = p.kmax > 2 && warps_for(2) <= 16 && p.uniform_rb && p.xsm && env_u32("QW_WIDE", 1);
+  if (p.wide) p.kmax = 2;
   p.warps = warps_for(p.kmax);
   p.warps2 = (c2 + p.kmax - 1) / p.kmax;
   p.teams = 1;
-  p.uniform_rb = (G.group2 % kRowsPerQuad) == 0;
   p.uq = quads_per_slot(p.kmax, p.uniform_rb);
-  p.xsm = G.cols <= 12288;
   p.rb_one = G.group2 == 1;
   p.rb_magic = p.rb_one ? 0u : (uint32_t)((0x100000000ull + G.group2 - 1) / G.group2);
   return 0;
@@ -725,7 +798,7 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   const size_t so_bytes = (size_t)so_rows_max * G.G2s * 4;
   const size_t part_bytes = (size_t)p.nq_max * p.warps * 16;  // [row][warp of a team]
   const size_t misc_bytes = (size_t)p.nq_max * 4 * 4 + ((size_t)p.nq_max * 4 + 4) * 4 + 256 * 4 + 64 * 4;
-  const size_t x_bytes = p.xsm ? align_up((size_t)G.cols * 4, 16) : 0;
+  const size_t x_bytes = p.xsm ? align_up((size_t)G.cols * 4 + 4, 16) : 0;  // + the pads' zero slot
   const uint32_t tmax = (p.kmax <= 2 && p.uniform_rb && p.xsm && p.uq == 2) ? 2u : 1u;
   const size_t win_bytes = (size_t)p.warps * tmax * kWinWords * 4;
   const size_t fixed = align_up(so_bytes, 16) + part_bytes + align_up(misc_bytes, 16) + x_bytes +
@@ -737,8 +810,9 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   const size_t unit_bytes = (size_t)p.uq * G.dense_bytes;
   const size_t units = (p.nq_max + p.uq - 1) / p.uq;
   // long ranges (group launches, big layers): two teams, the whole SM
-  p.teams = (p.nq_max >= env_u32("QW_TEAMS_MIN_NQ", 12) && p.kmax <= 2 && p.uniform_rb && p.xsm && p.uq == 2) ? 2 : 1;
-  const size_t half_sm = (p.teams == 2 ? 200 : env_u32("QW_SMEM_KB", 112)) * 1024, full_sm = 220 * 1024;
+  p.teams = (!p.wide && p.nq_max >= env_u32("QW_TEAMS_MIN_NQ", 12) && p.kmax <= 2 && p.uniform_rb && p.xsm &&
+             p.uq == 2) ? 2 : 1;
+  const size_t half_sm = (p.teams == 2 || p.wide ? 200 : env_u32("QW_SMEM_KB", 112)) * 1024, full_sm = 220 * 1024;
   size_t S = units;
   auto total_b = [&](size_t s) {
     return align_up(s * unit_bytes, 128) + fixed + pre_bytes(s) + (2 * s + 2) * 8;
@@ -819,10 +893,14 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   a.grid = p.grid, a.nq_max = p.nq_max, a.rb_magic = p.rb_magic, a.rb_one = p.rb_one;
   a.so_off = p.so_off, a.part_off = p.part_off, a.csr_off = p.misc_off, a.x_off = p.xg_off, a.win_off = p.win_off, a.pre_off = p.pre_off;
   a.bar_off = p.bar_off;
+  a.pf_n = env_u32("QW_NO_PF", 0) ? 0u : p.pf_n;
+  a.pf_late = env_u32("QW_PF_LATE", 1);
+  for (uint32_t r = 0; r < GemvPlan::kMaxPf; ++r) a.pf_ptr[r] = p.pf_ptr[r], a.pf_bytes[r] = p.pf_bytes[r];
   a.dbg = dbg;
   a.dbg_global = global_clock;
   a.wait_x = (flags & kXIndependent) ? 0u : 1u;
   a.pre = 1;
+  a.x_first = env_u32("QW_XFIRST", 0);
   if (const char* e = std::getenv("QW_NO_PRE")) a.pre = std::atoi(e) ? 0u : 1u;
   a.repeat = repeat;
   std::copy(p.cta_seg, p.cta_seg + p.grid, a.cta_seg);
@@ -830,7 +908,7 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   std::copy(p.cta_q1, p.cta_q1 + p.grid, a.cta_q1);
   std::copy(p.cta_e0, p.cta_e0 + p.grid, a.cta_e0);
   std::copy(p.cta_e1, p.cta_e1 + p.grid, a.cta_e1);
-  const GemvFn fn = p.teams == 2 ? pick_teams(p.kmax) : pick_kernel(p.kmax, p.uniform_rb, p.xsm);
+  const GemvFn fn = (p.teams == 2 || p.wide) ? pick_teams(p.kmax) : pick_kernel(p.kmax, p.uniform_rb, p.xsm);
   const uint32_t threads = (p.warps * p.teams + 2) * 32;
   void* params[] = {&a};
   return (int)launch_ex((const void*)fn, dim3(p.grid), dim3(threads), p.smem, (cudaStream_t)stream, pdl, params);

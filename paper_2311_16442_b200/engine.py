@@ -181,8 +181,17 @@ class DeviceLayer:
         out.layer_cfg = getattr(self, "layer_cfg", None)
         return out
 
+    def set_prefetch(self, next_layers: list["DeviceLayer"]) -> None:
+        """Decode chains: launches of this layer also stream `next_layers`'
+        weights (the following launch on the stream) into L2.  [] clears."""
+        check(lib().qw_layer_set_prefetch(self._h, _handles(next_layers), len(next_layers)))
+
     def launches_per_matvec(self, batch: int = 1) -> int:
         return int(lib().qw_launches_per_matvec(self._h, batch))
+
+
+def _handles(layers):
+    return (C.c_void_p * max(1, len(layers)))(*[d._h.value if hasattr(d._h, "value") else d._h for d in layers])
 
 
 def upload(layer: PackedLayer, device: int = 0) -> DeviceLayer:
@@ -212,6 +221,11 @@ class LayerGroup:
             self.close()
         except Exception:
             pass
+
+    def set_prefetch(self, next_layers: list["DeviceLayer"]) -> None:
+        """Decode chains: this group's launches also stream `next_layers`'
+        weights into L2 (see DeviceLayer.set_prefetch)."""
+        check(lib().qw_group_set_prefetch(self._h, _handles(next_layers), len(next_layers)))
 
     def matvec(self, x, outs=None, stream=None, pdl: bool = False, x_independent: bool = False):
         """x: cuda fp32 [cols] (original order); returns one [rows] output per layer."""

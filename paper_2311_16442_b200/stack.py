@@ -31,12 +31,14 @@ class _Slot:
 class LinearStack:
     def __init__(self, layers: list[DeviceLayer], device: int = 0, batch: int = 1,
                  pdl: bool = True, depends: list[bool] | None = None,
-                 groups: list[list[int]] | None = None):
+                 groups: list[list[int]] | None = None, prefetch: bool = False):
         """groups: consecutive index lists of linears that read the same input
         (q/k/v, gate/up) and run as ONE fused launch (batch 1); default one
         launch per linear.  depends[i] (per launch): launch i reads an input
         produced by launch i-1 (it waits for it); False lets it read its input
-        at once (it came from the host or an earlier, finished kernel)."""
+        at once (it came from the host or an earlier, finished kernel).
+        prefetch: each launch streams the next launch's weights into L2
+        (qw_*_set_prefetch), so HBM never idles between dependent launches."""
         self.device, self.batch, self.pdl = device, batch, pdl
         self.groups = groups if groups is not None else [[i] for i in range(len(layers))]
         assert [i for g in self.groups for i in g] == list(range(len(layers))), "groups must tile the layers in order"
@@ -44,6 +46,9 @@ class LinearStack:
         self.fused = [LayerGroup([layers[i] for i in g]) if len(g) > 1 and batch == 1 else None
                       for g in self.groups]
         self.dev = torch.device(f"cuda:{device}")
+        self.prefetch = prefetch and batch == 1
+        self._layers = layers
+        self.set_prefetch()
         xo = yo = 0
         self.slots = []
         for dl in layers:
@@ -58,6 +63,24 @@ class LinearStack:
         self.ws = Workspace(device, max_cols, batch)
         self.graph = None
         self.gemv_graph = None
+
+    def set_prefetch(self, select=None):
+        """Every launch (of those whose first layer `select` accepts) streams the
+        following launch's weights into L2 -- the last one the first's, i.e. the
+        next decode step.  Launch parameters are captured by value, so a graph
+        keeps the setting it was captured with."""
+        if not self.prefetch:
+            return
+        order = []  # launches in stream order: (fused group | layer, its layers)
+        for gi, g in enumerate(self.groups):
+            if select is not None and not select(self._layers[g[0]]):
+                continue
+            if self.fused[gi] is not None:
+                order.append((self.fused[gi], [self._layers[i] for i in g]))
+            else:
+                order.extend((self._layers[i], [self._layers[i]]) for i in g)
+        for k, (launch, _) in enumerate(order):
+            launch.set_prefetch(order[(k + 1) % len(order)][1])
 
     # ------------------------------------------------------------ views
     def x_of(self, i: int):
@@ -102,12 +125,14 @@ class LinearStack:
         return g
 
     def capture_subset(self, select):
+        self.set_prefetch(select)
         self.launch_subset(select)
         torch.cuda.synchronize(self.dev)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             self.launch_subset(select)
         torch.cuda.synchronize(self.dev)
+        self.set_prefetch()
         return g
 
     def replay(self):

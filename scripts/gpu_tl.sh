@@ -1,4 +1,4 @@
-cd $GRAFT_REPO_ROOT; python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-timeout 300 python scripts/timeline.py 4096 4096 1 2>&1 | tail -22
-timeout 300 python scripts/timeline.py 4096 4096 20 2>&1 | grep repeat
-timeout 300 python scripts/timeline.py 4096 11008 20 2>&1 | grep repeat
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -c 400 gpurun_out/bench.json

@@ -1,6 +1,6 @@
 """Global-clock timeline of a grouped decode chain (q/k/v group, o, gate/up
 group, down) x L decoder layers, CUDA graph + PDL (diagnostic).
-usage: python scripts/step_timeline.py [L]"""
+usage: python scripts/step_timeline.py [L] [pf]"""
 import ctypes as C
 import sys
 from pathlib import Path
@@ -24,6 +24,9 @@ for l in range(L):
         x = torch.from_numpy(qw.synth_activation(c, 8)).cuda()
         ys = [torch.empty(r, device="cuda") for _ in range(n)]
         launches.append((names[i], grp, dls, x, ys))
+if len(sys.argv) > 2 and sys.argv[2] == "pf":  # each launch prefetches the next one's weights into L2
+    for k, (nm, grp, dls, x, ys) in enumerate(launches):
+        grp.set_prefetch(launches[(k + 1) % len(launches)][2])
 E = lib().qw_debug_timeline_events()
 G = 448
 st = torch.zeros(len(launches), G * E, dtype=torch.int64, device="cuda")
@@ -48,10 +51,19 @@ for _ in range(3):
 torch.cuda.synchronize()
 a = st.cpu().numpy().reshape(len(launches), G, E).astype(np.int64)
 t0 = a[0, :, 0][a[0, :, 0] > 0].min()
-print("launch      entry0  dep_max    x_max  prolog_max  cons_min  cons_max    y_max   (ns from first entry)")
-prev = None
+ev = {"entry": 0, "dep": 1, "xind": 8, "x": 7, "gath": 9, "prolog": 2, "cons": 4, "csr": 6, "y": 5}
+print("per launch: median / max over CTAs (us from the previous launch's last y store)")
+print("launch   " + " ".join(f"{k:>12s}" for k in ev))
+prev_y = None
 for k, (nm, *_rest) in enumerate(launches):
     r = a[k]
     r = r[r[:, 0] > 0] - t0
-    print(f"{nm:9s} {r[:, 0].min():8d} {r[:, 1].max():8d} {r[:, 7].max():8d} {r[:, 2].max():10d} "
-          f"{r[:, 4].min():9d} {r[:, 4].max():9d} {r[:, 5].max():8d}")
+    if prev_y is None:
+        prev_y = r[:, 0].min()
+    cols = []
+    for name, e in ev.items():
+        v = r[:, e]
+        v = v[v > -t0]
+        cols.append(f"{(np.median(v) - prev_y) / 1e3:5.2f}/{(v.max() - prev_y) / 1e3:5.2f}")
+    print(f"{nm:8s} " + " ".join(f"{c:>12s}" for c in cols))
+    prev_y = r[:, 5].max()

@@ -19,8 +19,8 @@ x = torch.from_numpy(qw.synth_activation(cols, 8)).cuda()
 y = torch.empty(rows, device="cuda")
 E = lib().qw_debug_timeline_events()
 grid = dl.info["quads"] if dl.info["quads"] < 148 else 148
-names = ["entry", "copies issued", "prologue done", "first quad", "consumers done", "y written",
-         "csr done", "-"]
+names = ["entry", "dep resolved", "prologue done", "first unit in", "consumers done", "y written",
+         "outliers done", "x landed", "x-indep done", "gathered", "-", "-"]
 for trial in range(2):
     st = torch.zeros(grid * E, dtype=torch.int64, device="cuda")
     for _ in range(3):  # warm
@@ -29,6 +29,11 @@ for trial in range(2):
                                   C.c_void_p(st.data_ptr()), REP, 0,
                                   C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     torch.cuda.synchronize()
+    if trial == 0:
+        import oracle
+        ref = oracle.matvec_f64(layer, x.cpu().numpy())
+        yy = y.cpu().numpy()
+        print("  rel-L2 after the diagnostic launch:", float(np.linalg.norm(yy - ref) / np.linalg.norm(ref)))
     a = st.cpu().numpy().reshape(grid, E).astype(np.int64)
     d = a - a[:, :1]
     print(f"trial {trial}: cycles from entry (mean / max over CTAs)")

@@ -263,3 +263,21 @@ def test_group_rejects_mismatched_geometry():
     b = qw.DeviceLayer(qw.synth_layer(64, 1024, seed=2))
     with pytest.raises(qw.QWeightError):
         qw.LayerGroup([a, b])
+
+
+def test_prefetch_hint_leaves_results_unchanged():
+    """qw_*_set_prefetch: a launch that also streams the next launch's weights
+    into L2 computes bitwise the same outputs."""
+    torch = _torch()
+    la, lb = qw.synth_layer(512, 1024, seed=70), qw.synth_layer(256, 1024, seed=71)
+    a, b = qw.DeviceLayer(la), qw.DeviceLayer(lb)
+    grp = qw.LayerGroup([qw.DeviceLayer(qw.synth_layer(512, 1024, seed=72 + i)) for i in range(2)])
+    xd = torch.from_numpy(qw.synth_activation(1024, 73)).cuda()
+    ya, yg = a.matvec(xd).cpu().numpy(), [o.cpu().numpy() for o in grp.matvec(xd)]
+    a.set_prefetch([b])
+    grp.set_prefetch([a, b])
+    assert np.array_equal(a.matvec(xd).cpu().numpy(), ya)
+    assert all(np.array_equal(o.cpu().numpy(), r) for o, r in zip(grp.matvec(xd), yg))
+    a.set_prefetch([])
+    with pytest.raises(qw.QWeightError):
+        a.set_prefetch([b] * 5)
