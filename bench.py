@@ -255,6 +255,9 @@ def run_ours(args):
     n_gemv = len(per_layer)
     prep_s = time.perf_counter() - t_prep
 
+    chain = args.launch == "chain"
+    if chain:
+        stack.use_chain(True)  # the whole step as one persistent kernel
     # correctness spot check of the captured path before timing
     stack.capture()
     stack.replay()
@@ -294,17 +297,33 @@ def run_ours(args):
     clocks = clk.summary()
 
     # ---- the same step with every GEMV's input independent of its predecessor
-    # (no dependency wait: consecutive GEMVs overlap; kernel-stream throughput)
-    stack.depends = [False] * len(stack.groups)
-    g_ind = stack.capture_subset(lambda d: True)
-    ms_ind = timed(g_ind.replay, args.steps, args.warmup)
-    stack.depends = [True] * len(stack.groups)
+    # (no dependency wait; kernel-stream throughput)
+    if chain:
+        ch_ind = stack.make_chain([False] * len(stack.groups))
+        ms_ind = timed(ch_ind.run, args.steps, args.warmup)
+        del ch_ind
+    else:
+        stack.depends = [False] * len(stack.groups)
+        g_ind = stack.capture_subset(lambda d: True)
+        ms_ind = timed(g_ind.replay, args.steps, args.warmup)
+        stack.depends = [True] * len(stack.groups)
 
-    # ---- dominant kernel alone: fused GEMV on the q/k/v/o shape
+    # ---- the other execution of the same dependent step: one fused GEMV launch
+    # per group (graph + PDL) when the headline is the chain kernel, and vice versa
+    saved, stack.chain = stack.chain, None
+    if chain:
+        g_launch = stack.capture_subset(lambda d: True)
+        ms_launch = timed(g_launch.replay, args.steps, args.warmup)
+    else:
+        ch_dep = stack.make_chain()
+        ms_launch = timed(ch_dep.run, args.steps, args.warmup)
+        del ch_dep
+    # ... and its q/k/v/o launches alone
     sel = lambda d: d.rows == 4096 and d.cols == 4096  # noqa: E731
     g_q = stack.capture_subset(sel)
     n_q = sum(len(g) for g in stack.groups if sel(stack.slots[g[0]].layer))
     ms_q = timed(g_q.replay, args.steps, args.warmup)
+    stack.chain = saved
     q_bytes = b_alg(payload[0], 4096, 4096)
     us_q = ms_q * 1e3 / n_q
 
@@ -327,11 +346,18 @@ def run_ours(args):
     hbm_peak, peak_kind = peaks()
     value = world * step_bytes / (ms_step * 1e6)  # GB/s over all ranks
     achieved_q = q_bytes / (us_q * 1e3)
+    if chain:  # the dominant (only) kernel is the chain kernel: one launch per step
+        roof = {"achieved": step_bytes / (ms_step * 1e6), "kernel": "chain_kernel (persistent: the whole decode "
+                "step, 128 grouped GEMV steps)", "us_per_launch": ms_step * 1e3, "algorithmic_bytes": step_bytes}
+    else:
+        roof = {"achieved": achieved_q, "kernel": "gemv_kernel (fused dequant GEMV + CSR), q/k/v 4096x4096 group "
+                "launch", "us_per_launch": us_q, "algorithmic_bytes": q_bytes}
     prof = ROOT / "profiles" / "ncu_summary.json"
     traffic = None
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("gemv_q_proj", {}).get("dram_bytes_per_launch")
+            traffic = json.loads(prof.read_text()).get("chain_kernel" if chain else "gemv_q_proj", {}).get(
+                "dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -346,9 +372,16 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "fp16x2-dot/fp32-accumulate", "data": "synthetic",
             "us_per_layer": round(ms_step * 1e3 / n_gemv, 4),
-            "dependency": "decode chain: per decoder layer 4 launches -- {q,k,v} (one input, one "
-                          "fused launch), o, {gate,up} (one fused launch), down -- each waiting for "
-                          "its predecessor before reading x; weights of launch i+1 stream under launch i",
+            "dependency": "decode chain: per decoder layer 4 steps -- {q,k,v} (one input, fused), o, "
+                          "{gate,up} (fused), down -- each waiting for its predecessor before reading x" +
+                          ("; one persistent kernel, grid-wide step counters, weights of step s+1 stream "
+                           "under step s" if chain else "; one launch per step, programmatic dependent launch"),
+            ("per_launch" if chain else "chain_kernel"): {
+                "value": round(world * step_bytes / (ms_launch * 1e6), 2), "unit": "GB/s",
+                "us_per_layer": round(ms_launch * 1e3 / n_gemv, 4),
+                "note": ("same dependent chain, one fused GEMV launch per step (CUDA graph + PDL)" if chain else
+                         "same dependent chain as ONE persistent kernel (qw_chain_*: grid-wide step counters, "
+                         "one weight ring across the steps)")},
             "independent": {"value": round(world * step_bytes / (ms_ind * 1e6), 2), "unit": "GB/s",
                             "us_per_layer": round(ms_ind * 1e3 / n_gemv, 4),
                             "note": "inputs independent of the previous GEMV: no wait, kernels overlap"},
@@ -358,20 +391,22 @@ def run_ours(args):
                        "alpha": ALPHA, "group1": 16, "group2": GROUP2, "outlier_ratio": RATIO,
                        "batch": 1, "bytes_per_step": step_bytes,
                        "l2": "inputs larger than L2 (distinct HBM copy per GEMV)",
-                       "launch": "CUDA graph, programmatic dependent launch" if not args.no_pdl
-                                 else "CUDA graph",
+                       "launch": ("CUDA graph: counter reset + one persistent chain kernel" if chain else
+                                  "CUDA graph, programmatic dependent launch" if not args.no_pdl else "CUDA graph"),
                        "prefetch": "none" if not args.prefetch else
                                    "each launch streams the next launch's weights HBM->L2 (read once per step)"},
-            "roofline": {"bound": "hbm", "achieved": round(achieved_q, 2), "peak": hbm_peak,
-                         "unit": "GB/s", "frac": round(achieved_q / hbm_peak, 4),
-                         "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "gemv_kernel (fused dequant GEMV + CSR), q/k/v 4096x4096 group launch",
-                         "us_per_launch": round(us_q, 4), "algorithmic_bytes": q_bytes},
+            "roofline": {"bound": "hbm", "achieved": round(roof["achieved"], 2), "peak": hbm_peak,
+                         "unit": "GB/s", "frac": round(roof["achieved"] / hbm_peak, 4),
+                         "traffic": traffic, "peak_kind": peak_kind, "kernel": roof["kernel"],
+                         "us_per_launch": round(roof["us_per_launch"], 4),
+                         "algorithmic_bytes": roof["algorithmic_bytes"],
+                         "qkvo_group_launch": {"achieved": round(achieved_q, 2), "us_per_launch": round(us_q, 4),
+                                               "algorithmic_bytes": q_bytes}},
             "e2e": {"value": round(world * step_bytes / (e2e_ms * 1e6), 2), "unit": "GB/s",
                     "h2d_bytes_per_step": stack.h2d_bytes, "d2h_bytes_per_step": stack.d2h_bytes,
                     "ms_per_step": round(e2e_ms, 4),
                     "api": "LinearStack.run (pinned H2D, graph, D2H, sync)"},
-            "gpu_launches": len(stack.groups) * args.steps,
+            "gpu_launches": (1 if chain else len(stack.groups)) * args.steps,
             "clocks": clocks,
             "prep_s": round(prep_s, 1),
         }
@@ -391,6 +426,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=32, help="decoder layers per step")
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--launch", default="graph", choices=["chain", "graph"],
+                    help="chain: the decode step as one persistent kernel; graph: one launch per step")
     ap.add_argument("--prefetch", action="store_true", help="L2 prefetch of the next launch's weights")
     ap.add_argument("--ungrouped", action="store_true", help="one launch per linear (no q/k/v, gate/up fusion)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")

@@ -196,6 +196,28 @@ int qw_group_matvec(const qw_group* group, const float* x, float* const* ys, voi
  * n = 0 clears.  The next layers must outlive the setting. */
 int qw_layer_set_prefetch(qw_layer* layer, const qw_layer* const* next, uint32_t n);
 int qw_group_set_prefetch(qw_group* group, const qw_layer* const* next, uint32_t n);
+/* Decode chain (batch 1): a fixed sequence of launch steps -- each a group of
+ * 1..4 layers of identical geometry reading one activation x -- executed by
+ * ONE persistent kernel: one CTA per SM streams the packed weights of all
+ * steps through a single shared-memory ring (step s+1's weights land while
+ * step s computes), and a step with depends != 0 reads x only after every CTA
+ * stored its outputs of the previous step (a grid-wide counter replaces the
+ * kernel boundary).  Buffers are bound at creation; qw_chain_run launches the
+ * whole sequence (a counter reset + 1 kernel, CUDA-graph capturable).
+ * Results equal the per-step launches' (qw_group_matvec / qw_matvec_ex).
+ * QW_ERR_UNSUPPORTED: a step geometry the chain kernel does not cover
+ * (group2 % 4 != 0, more than 12288 columns). */
+typedef struct qw_chain qw_chain;
+typedef struct {
+  const qw_layer* const* layers; /* n layers, identical geometry */
+  uint32_t n;
+  const float* x;                /* device fp32 [cols], original channel order */
+  float* const* ys;              /* device fp32 [rows] per layer */
+  uint32_t depends;              /* x is produced by the previous step */
+} qw_chain_step;
+int qw_chain_create(const qw_chain_step* steps, uint32_t n, qw_chain** out);
+int qw_chain_run(const qw_chain* chain, void* stream);
+int qw_chain_free(qw_chain* chain);
 /* Host-buffer, synchronous, checked: length and finiteness as the reference
  * (engine.cpp:124-132).  x_len must equal batch * cols. */
 int qw_matvec_host(const qw_layer* layer, const float* x, uint64_t x_len,

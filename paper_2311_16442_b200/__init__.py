@@ -14,12 +14,13 @@ __all__ = [
     "payload_bytes", "permute", "plant_outliers", "quantize_layer", "read_packed_layer",
     "shard_rows", "shard_tiles", "synth_activation", "synth_calibration", "synth_gaussian",
     "synth_layer", "validate_layer", "write_packed_layer", "DeviceLayer", "Workspace",
-    "MatvecResult", "upload", "LayerGroup",
+    "MatvecResult", "upload", "LayerGroup", "DecodeChain",
 ]
 
 
 def __getattr__(name):  # the engine imports torch lazily
-    if name in ("DeviceLayer", "Workspace", "MatvecResult", "upload", "default_workspace", "LayerGroup"):
+    if name in ("DeviceLayer", "Workspace", "MatvecResult", "upload", "default_workspace", "LayerGroup",
+                "DecodeChain"):
         from . import engine
         return getattr(engine, name)
     raise AttributeError(name)

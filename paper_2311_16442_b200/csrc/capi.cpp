@@ -53,6 +53,12 @@ struct qw_group {
   int device = 0;
 };
 
+struct qw_chain {
+  qwdev::ChainPlan* plan = nullptr;
+  int device = 0;
+  ~qw_chain() { qwdev::free_chain(plan); }
+};
+
 struct qw_workspace {
   qwdev::Workspace ws;
 };
@@ -786,6 +792,54 @@ int qw_layer_set_prefetch(qw_layer* L, const qw_layer* const* next, uint32_t n) 
 int qw_group_set_prefetch(qw_group* g, const qw_layer* const* next, uint32_t n) {
   if (!g) return fail(QW_ERR_ARG, "prefetch: null group");
   return set_prefetch(g->plan, g->device, next, n);
+}
+
+int qw_chain_create(const qw_chain_step* steps, uint32_t n, qw_chain** out) {
+  return guarded([&] {
+    if (!steps || !out || n == 0) return fail(QW_ERR_ARG, "chain: null argument");
+    std::vector<qwdev::ChainStepDesc> d(n);
+    std::vector<std::vector<const qwdev::DeviceLayer*>> lay(n);
+    std::vector<std::vector<const uint32_t*>> rps(n);
+    const int device = steps[0].n && steps[0].layers && steps[0].layers[0] ? steps[0].layers[0]->device : 0;
+    int num_sms = 148;
+    for (uint32_t s = 0; s < n; ++s) {
+      const qw_chain_step& st = steps[s];
+      if (!st.layers || !st.ys || !st.x || st.n == 0) return fail(QW_ERR_ARG, "chain: null step field");
+      if (st.n > qwdev::kMaxSeg) return fail(QW_ERR_UNSUPPORTED, "chain: at most 4 layers per step");
+      for (uint32_t l = 0; l < st.n; ++l) {
+        if (!st.layers[l] || !st.ys[l]) return fail(QW_ERR_ARG, "chain: null layer or output");
+        if (st.layers[l]->device != device) return fail(QW_ERR_ARG, "chain: layers on different devices");
+        lay[s].push_back(&st.layers[l]->dev);
+        rps[s].push_back(st.layers[l]->host_row_ptr.data());
+        num_sms = st.layers[l]->num_sms;
+      }
+      d[s] = qwdev::ChainStepDesc{lay[s].data(), rps[s].data(), st.n, st.x, st.ys, st.depends};
+    }
+    cudaSetDevice(device);
+    auto C = std::make_unique<qw_chain>();
+    C->device = device;
+    const int e = qwdev::plan_chain(&C->plan, d.data(), n, num_sms);
+    if (e == (int)cudaErrorInvalidValue) return fail(QW_ERR_ARG, "chain: a step's layers differ in geometry");
+    if (e == (int)cudaErrorNotSupported)
+      return fail(QW_ERR_UNSUPPORTED, "chain: step geometry not covered (group2 % 4 != 0 or > 12288 columns)");
+    if (e) return cuda_fail((cudaError_t)e, "chain plan");
+    *out = C.release();
+    return (int)QW_OK;
+  });
+}
+
+int qw_chain_run(const qw_chain* c, void* stream) {
+  if (!c) return fail(QW_ERR_ARG, "chain: null");
+  int dev_now = -1;
+  cudaGetDevice(&dev_now);
+  if (dev_now != c->device) cudaSetDevice(c->device);
+  const int e = qwdev::launch_chain(c->plan, stream);
+  return e ? cuda_fail((cudaError_t)e, "chain launch") : QW_OK;
+}
+
+int qw_chain_free(qw_chain* c) {
+  delete c;
+  return QW_OK;
 }
 
 int qw_debug_group_timeline(const qw_group* g, const float* x, float* const* ys, unsigned long long* stamps,

@@ -135,4 +135,24 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
 int launch_unpack(const DeviceLayer& L, uint8_t* codes2, uint8_t* zeros2, uint8_t* scodes,
                   uint8_t* codes4, void* stream);
 
+// Decode chain (batch 1): a sequence of launch steps (each a group of 1..4
+// layers of identical geometry reading one activation) run by ONE persistent
+// kernel -- one CTA per SM streams the weights of step s+1 into its ring
+// while step s computes; a step that depends on its predecessor waits on a
+// grid-wide completion counter instead of a kernel boundary.
+struct ChainStepDesc {
+  const DeviceLayer* const* layers;
+  const uint32_t* const* host_row_ptrs;
+  uint32_t n;
+  const float* x;     // device fp32 [cols]
+  float* const* ys;   // device fp32 [rows] per layer
+  uint32_t depends;   // x is produced by the previous step: wait for it
+};
+struct ChainPlan;
+// cudaErrorInvalidValue: a step's layers differ in geometry;
+// cudaErrorNotSupported: a geometry the chain kernel does not cover.
+int plan_chain(ChainPlan** out, const ChainStepDesc* steps, uint32_t n, int num_sms);
+int launch_chain(const ChainPlan* p, void* stream);
+void free_chain(ChainPlan* p);
+
 }  // namespace qwdev

@@ -190,6 +190,53 @@ class DeviceLayer:
         return int(lib().qw_launches_per_matvec(self._h, batch))
 
 
+class _ChainStep(C.Structure):
+    _fields_ = [("layers", C.POINTER(C.c_void_p)), ("n", C.c_uint32), ("x", C.c_void_p),
+                ("ys", C.POINTER(C.c_void_p)), ("depends", C.c_uint32)]
+
+
+class DecodeChain:
+    """A fixed sequence of batch-1 launch steps run by ONE persistent kernel
+    (qw_chain_*): steps = [(layers, x, ys, depends)], layers of a step share
+    geometry and read x (cuda fp32 [cols]); ys[i] receives layers[i] @ x;
+    depends: x is the previous step's output (wait for every CTA's stores)."""
+
+    def __init__(self, steps):
+        self._keep = []
+        arr = (_ChainStep * len(steps))()
+        for i, (layers, x, ys, dep) in enumerate(steps):
+            if len(layers) != len(ys):
+                raise QWeightError(1, "chain: one output per layer")
+            for o in ys:
+                if o.dtype != torch.float32 or not o.is_cuda or not o.is_contiguous():
+                    raise QWeightError(1, "chain: outputs must be contiguous cuda float32")
+            if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous() or x.numel() != layers[0].cols:
+                raise QWeightError(1, "chain: x must be a contiguous cuda float32 [cols]")
+            lh = _handles(layers)
+            yh = (C.c_void_p * len(ys))(*[o.data_ptr() for o in ys])
+            self._keep += [lh, yh, layers, x, ys]
+            arr[i] = _ChainStep(C.cast(lh, C.POINTER(C.c_void_p)), len(layers), x.data_ptr(),
+                                C.cast(yh, C.POINTER(C.c_void_p)), 1 if dep else 0)
+        h = C.c_void_p()
+        check(lib().qw_chain_create(C.cast(arr, C.c_void_p), len(steps), C.byref(h)))
+        self._h = h
+        self.steps = len(steps)
+
+    def run(self, stream=None) -> None:
+        check(lib().qw_chain_run(self._h, C.c_void_p(_stream_handle(stream))))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().qw_chain_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def _handles(layers):
     return (C.c_void_p * max(1, len(layers)))(*[d._h.value if hasattr(d._h, "value") else d._h for d in layers])
 

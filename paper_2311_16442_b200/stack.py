@@ -13,7 +13,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .engine import DeviceLayer, LayerGroup, Workspace
+from .engine import DecodeChain, DeviceLayer, LayerGroup, Workspace
 
 try:
     import torch
@@ -63,6 +63,7 @@ class LinearStack:
         self.ws = Workspace(device, max_cols, batch)
         self.graph = None
         self.gemv_graph = None
+        self.chain = None
 
     def set_prefetch(self, select=None):
         """Every launch (of those whose first layer `select` accepts) streams the
@@ -103,7 +104,31 @@ class LinearStack:
                                        workspace=self.ws, stream=stream, pdl=self.pdl,
                                        x_independent=(not dep) or k > 0)
 
+    def make_chain(self, depends: list[bool] | None = None) -> DecodeChain:
+        """The whole step as ONE persistent kernel (qw_chain_*, batch 1): one
+        chain step per launch of the grouped sequence; depends per launch."""
+        assert self.batch == 1, "the decode chain is batch 1"
+        dep = self.depends if depends is None else depends
+        steps = []
+        for gi, g in enumerate(self.groups):
+            lay = [self.slots[i].layer for i in g]
+            if self.fused[gi] is not None:
+                steps.append((lay, self.x_of(g[0])[0], [self.y_of(i)[0] for i in g], dep[gi]))
+            else:
+                for k, i in enumerate(g):
+                    src = g[0] if len(g) > 1 else i
+                    steps.append(([self.slots[i].layer], self.x_of(src)[0], [self.y_of(i)[0]], dep[gi] and k == 0))
+        return DecodeChain(steps)
+
+    def use_chain(self, on: bool = True):
+        """launch_step / capture / run go through the persistent decode-chain kernel."""
+        self.chain = self.make_chain() if on else None
+        self.graph = None
+
     def launch_step(self, stream=None):
+        if self.chain is not None:
+            self.chain.run(stream)
+            return
         for gi in range(len(self.groups)):
             self._launch(gi, stream)
 

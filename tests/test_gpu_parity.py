@@ -281,3 +281,58 @@ def test_prefetch_hint_leaves_results_unchanged():
     a.set_prefetch([])
     with pytest.raises(qw.QWeightError):
         a.set_prefetch([b] * 5)
+
+
+def test_decode_chain_true_dependency():
+    """qw_chain: step s reads the y of step s-1 written by other CTAs of the
+    same persistent kernel (grid-wide counter); each output equals the
+    single-layer launch on the same input and the f64 oracle."""
+    torch = _torch()
+    la = qw.synth_layer(1024, 1024, seed=80, outlier_ratio=0.005)
+    lb = [qw.synth_layer(512, 1024, seed=81 + i, outlier_ratio=0.005) for i in range(2)]
+    lc = qw.synth_layer(256, 512, seed=83, group2=4)
+    A, B, Cc = qw.DeviceLayer(la), [qw.DeviceLayer(L) for L in lb], qw.DeviceLayer(lc)
+    x = torch.from_numpy(qw.synth_activation(1024, 84)).cuda()
+    ya = torch.zeros(1024, device="cuda")
+    yb = [torch.zeros(512, device="cuda") for _ in range(2)]
+    yc = torch.zeros(256, device="cuda")
+    ch = qw.DecodeChain([([A], x, [ya], False), (B, ya, yb, True), ([Cc], yb[1], [yc], True)])
+    for _ in range(3):  # counters reset per run
+        for t in (ya, *yb, yc):
+            t.zero_()
+        ch.run()
+        torch.cuda.synchronize()
+        ra = A.matvec(x)
+        assert torch.equal(ya, ra)
+        for d, o in zip(B, yb):
+            assert torch.equal(o, d.matvec(ra))
+        assert torch.equal(yc, Cc.matvec(yb[1]))
+    xa = x.cpu().numpy()
+    assert rel_l2(ya.cpu().numpy(), oracle.matvec_f64(la, xa)) <= TOL
+
+
+def test_decode_chain_llama_shapes_match_group_launches():
+    torch = _torch()
+    shapes = [(4096, 4096, 3), (4096, 4096, 1), (11008, 4096, 2), (4096, 11008, 1)]
+    steps, ref = [], []
+    for i, (r, c, n) in enumerate(shapes):
+        dls = [qw.DeviceLayer(qw.synth_layer(r, c, seed=90 + 4 * i + j)) for j in range(n)]
+        x = torch.from_numpy(qw.synth_activation(c, 95 + i)).cuda()
+        ys = [torch.zeros(r, device="cuda") for _ in range(n)]
+        steps.append((dls, x, ys, i > 0))
+        ref.append(qw.LayerGroup(dls).matvec(x) if n > 1 else [dls[0].matvec(x)])
+    ch = qw.DecodeChain(steps)
+    ch.run()
+    torch.cuda.synchronize()
+    for (dls, x, ys, _), rs in zip(steps, ref):
+        for y, r in zip(ys, rs):
+            assert rel_l2(y.cpu().numpy(), r.cpu().numpy()) <= 1e-6
+
+
+def test_decode_chain_rejects_unsupported_geometry():
+    torch = _torch()
+    d = qw.DeviceLayer(qw.synth_layer(64, 512, seed=1, group2=5))
+    x, y = torch.zeros(512, device="cuda"), torch.zeros(64, device="cuda")
+    with pytest.raises(qw.QWeightError) as ei:
+        qw.DecodeChain([([d], x, [y], False)])
+    assert ei.value.status == 5
