@@ -356,8 +356,12 @@ def run_ours(args):
     traffic = None
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("chain_kernel" if chain else "gemv_q_proj", {}).get(
-                "dram_bytes_per_launch")
+            summ = json.loads(prof.read_text())
+            if chain:
+                per = summ.get("chain_kernel", {}).get("dram_bytes_per_decoder_layer")
+                traffic = per * args.layers if per else None
+            else:
+                traffic = summ.get("gemv_q_proj", {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
