@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "qw_device.hpp"
@@ -58,7 +59,10 @@ constexpr uint32_t kBStageBytes = kStageK * 16 * 2;  // 4 KB: 8 slabs of 16 k x 
 // over 8 tiles (wide rows keep the TMA request count low), plus the 2-order
 // params of the tile's row blocks [<= 33][24 groups] (read from shared memory:
 // a global load in flight would stall the async-proxy fence that publishes A)
-constexpr uint32_t kBoxC2 = 96, kBoxMeta = 16, kBoxC4 = 64, kBoxS4 = 16, kBoxZ4 = 4;  // u32
+// Box widths: the fields a sub-stage needs (96, 16, 64, 16, 4 u32) padded so
+// the quad rows of a box sit at bank-spread strides (dequant lane = quad):
+// conflict-free 16-byte code loads, at most 2-way for the small fields.
+constexpr uint32_t kBoxC2 = 100, kBoxMeta = 20, kBoxC4 = 68, kBoxS4 = 20, kBoxZ4 = 8;  // u32
 constexpr uint32_t kSoBoxG = 24, kSoRowsMax = 33;
 constexpr uint32_t kOffC2 = 0, kOffMeta = kOffC2 + 32 * kBoxC2 * 4, kOffC4 = kOffMeta + 32 * kBoxMeta * 4,
                    kOffS4 = kOffC4 + 32 * kBoxC4 * 4, kOffZ4 = kOffS4 + 32 * kBoxS4 * 4,
@@ -66,6 +70,7 @@ constexpr uint32_t kOffC2 = 0, kOffMeta = kOffC2 + 32 * kBoxC2 * 4, kOffC4 = kOf
                    kWStageBytes = (kOffSo + kSoRowsMax * kSoBoxG * 4 + 1023) / 1024 * 1024;  // 28 KB
 constexpr uint32_t kWSlots = 2, kBSlots = 8, kABufs = 3;
 constexpr uint32_t kDqWarps = 16;
+constexpr uint32_t kDenseStride = 20;  // fp32 words per accumulator row in shared memory
 constexpr uint32_t kThreads = (2 + kDqWarps) * 32;
 
 // ---------------------------------------------------------------- PTX
@@ -220,7 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   uint64_t* dfull = aempty + kABufs;   // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dfull + 1);
   uint32_t* s_last = tmem_slot + 1;
-  float* s_dense = reinterpret_cast<float*>(s_last + 3);  // [128][17]
+  // [128][kDenseStride]: 16-byte rows so the split-K reduction reads float4s
+  float* s_dense = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_last + 3) + 15) & ~uintptr_t(15));
 
   const uint32_t tile = blockIdx.x / a.ks, split = blockIdx.x % a.ks;
   // K split over weight stages (8 tiles); sub-stages of 2 tiles feed the MMA
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const uint32_t ab = i % kABufs, ph = (i / kABufs) & 1u, bs = i % kBSlots;
         mbar_wait(&afull[ab], ph);
         mbar_wait(&bfull[bs], (i / kBSlots) & 1u);
-        if (i == 3) gstamp(a, 5);  // MMA thread: sub-stage 3's A and B ready
+
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t abase = smem_addr(sA + ab * kATileBytes), bbase = smem_addr(sB + bs * kBStageBytes);
 #pragma unroll
@@ -307,8 +313,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           smem_addr(dfull)));
     }
   } else {
-    // ---------------- dequant warps: item = (quad q, group j, channel half h) of a sub-stage
-    const uint32_t dt = threadIdx.x - 64, h = dt >> 8, q = (dt >> 3) & 31u, j = dt & 7u;
+    // ---------------- dequant warps: item = (quad q, group j, channel half h) of a sub-stage.
+    // Lane = quad; warps 2..13 take the 2-bit groups (j < 6), 14..17 the 4-bit
+    // ones, so no warp diverges over the two decode paths.
+    const uint32_t dw = warp - 2, q = lane;
+    const uint32_t j = dw < 12 ? dw >> 1 : 6 + ((dw - 12) >> 1), h = dw & 1u;
     const uint32_t quad = tile * kTileQuads + q;
     const uint32_t row0 = min(quad * 4, G.rows - 1);
     const uint32_t rb_local = (a.rb_one ? row0 : __umulhi(row0, a.rb_magic)) - rb_tile;
@@ -316,6 +325,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const uint32_t sub = j % 3;
     const uint32_t esh = sub == 0 ? 6u : (sub == 1 ? 10u : 13u), emask = sub == 0 ? 15u : 7u;
     const uint32_t eshl = sub == 0 ? 0u : 1u;
+    // (1024 + field) 2^eshl - 1024 2^eshl = eff, exactly (fp16 integers <= 2078 are even above 2048)
+    const half2 e2h = __float2half2_rn(eshl ? 2.0f : 1.0f), eoff = __float2half2_rn(eshl ? -2048.0f : -1024.0f);
+    const half2 h1024 = __float2half2_rn(1024.0f);
     const uint32_t a_item = (q & 1u) * 8 + (q >> 1) * kASbo + (2 * j + h) * kALbo;  // + (c % 8) * 16
     for (uint32_t i = 0; i < nsub; ++i) {
       const uint32_t wi = i / kSubPerW, s4i = i % kSubPerW, ws = wi % kWSlots, ab = i % kABufs;
@@ -329,20 +341,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const uint4 c = *reinterpret_cast<const uint4*>(w + kOffC2 + q * kBoxC2 * 4 + 16 * g6);
         const uint2 m = *reinterpret_cast<const uint2*>(w + kOffMeta + q * kBoxMeta * 4 + 8 * (g6 / 3));
         const half2 Sh = __float2half2_rn(half_bits_to_float(sc) * s2sc);  // scale2 2^(12-P)
-        const int zero2 = (int)(sc >> 16);
+        const half2 z2h = __float2half2_rn((float)(sc >> 16));                // zero2 (exact)
         const uint32_t mm[2] = {m.x, m.y}, cw[2] = {h ? c.y : c.x, h ? c.w : c.z};
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
           const uint32_t v = mm[p];
-          const int mA = (int)(((v >> esh) & emask) << eshl) - zero2;
-          const int mB = (int)(((v >> (16 + esh)) & emask) << eshl) - zero2;
-          const int zA = (int)((v >> (2 * sub)) & 3u), zB = (int)((v >> (16 + 2 * sub)) & 3u);
-          half2 M[4];
-          M[0] = as_h2(pack_h2((float)mA * 4096.0f, (float)mB * 4096.0f));
-          M[1] = __hmul2(M[0], __float2half2_rn(0.25f));
-          M[2] = __hmul2(M[1], __float2half2_rn(0.25f));
-          M[3] = __hmul2(M[2], __float2half2_rn(0.25f));
-          const half2 Z = as_h2(pack_h2((float)(-zA * mA) * (1.0f / 4096.0f), (float)(-zB * mB) * (1.0f / 4096.0f)));
+          // fp16 integers from 0x6400 (1024) | field, both rows at once, exact:
+          // mrow = eff - zero2 (eff = field << eshl), z = the group's 2-bit zero
+          const half2 e = __hfma2(as_h2(((v >> esh) & (emask | (emask << 16))) | 0x64006400u), e2h, eoff);
+          const half2 mrow = __hsub2(e, z2h);
+          const half2 zh = __hsub2(as_h2(((v >> (2 * sub)) & 0x00030003u) | 0x64006400u), h1024);
+          half2 M[4];  // mrow 2^(12 - 2b): c 2^(2b-24) * M[b] = c mrow 2^-12
+          M[0] = __hmul2(mrow, __float2half2_rn(4096.0f));
+          M[1] = __hmul2(mrow, __float2half2_rn(1024.0f));
+          M[2] = __hmul2(mrow, __float2half2_rn(256.0f));
+          M[3] = __hmul2(mrow, __float2half2_rn(64.0f));
+          const half2 Z = __hmul2(zh, __hmul2(mrow, __float2half2_rn(-1.0f / 4096.0f)));  // -z mrow 2^-12
 #pragma unroll
           for (int cc = 0; cc < 8; ++cc) {
             const uint32_t src = cc < 4 ? cw[p] : cw[p] >> 8;
@@ -362,8 +376,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const half2 M0 = __float2half2_rn(32768.0f), M1 = __float2half2_rn(2048.0f);  // 2^(15-b)
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-          const float zA = (float)((z4 >> (8 * p)) & 15u), zB = (float)((z4 >> (8 * p + 4)) & 15u);
-          const half2 Z = as_h2(pack_h2(-zA * (1.0f / 512.0f), -zB * (1.0f / 512.0f)));
+          // zeros of the row pair as fp16 integers (0x6400 | z - 1024), times -2^-9
+          const uint32_t zz = ((z4 >> (8 * p)) & 0xFu) | (((z4 >> (8 * p + 4)) & 0xFu) << 16);
+          const half2 Z = __hmul2(__hsub2(as_h2(zz | 0x64006400u), __float2half2_rn(1024.0f)),
+                                  __float2half2_rn(-1.0f / 512.0f));
           const half2 Sh = as_h2(pack_h2(half_bits_to_float(sw[p]) * s4sc, half_bits_to_float(sw[p] >> 16) * s4sc));
 #pragma unroll
           for (int cc = 0; cc < 8; ++cc) {
@@ -379,9 +395,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         __syncwarp();
         if (lane == 0) mbar_arrive(&wempty[ws]);
       }
-      if (threadIdx.x == 64 && i == 3) gstamp(a, 2);  // sub-stage 3 decoded (registers)
+
       if (i >= kABufs) mbar_wait(&aempty[ab], ((i / kABufs) - 1) & 1u);
-      if (threadIdx.x == 64 && i == 3) gstamp(a, 3);  // sub-stage 1's MMA done (A buffer free)
+
       uint8_t* at = sA + ab * kATileBytes + a_item;
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc)
@@ -389,10 +405,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&afull[ab]);
-      if (threadIdx.x == 64 && i == 3) gstamp(a, 4);  // sub-stage 3's A tile published
+
     }
     // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
     if (warp < 6) {
+      // the column scales (prologue output) are loaded while the last MMAs run
+      pdl_wait();
+      float csc[16];
+#pragma unroll
+      for (int n = 0; n < 16; ++n) csc[n] = p2(a.shift + __ldg(a.xexp + n));
       mbar_wait(dfull, 0);
       if (threadIdx.x == 64) gstamp(a, 7);  // accumulator ready
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -405,14 +426,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           : "r"(tmem + ((quarter * 32u) << 16)));
       asm volatile("tcgen05.wait::ld.sync.aligned;");
       const uint32_t t = quarter * 32 + lane;  // row within the tile
-      pdl_wait();  // xexp is the prologue kernel's output
 #pragma unroll
-      for (int n = 0; n < 16; ++n) s_dense[t * 17 + n] = __uint_as_float(r[n]) * p2(a.shift + a.xexp[n]);
+      for (int n = 0; n < 16; ++n) s_dense[t * kDenseStride + n] = __uint_as_float(r[n]) * csc[n];
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) gstamp(a, 2);  // CTA joined after the accumulator read
 
-  // dense part of this split is in s_dense[row][n] (row-major, padded stride 17)
+  // dense part of this split is in s_dense[row][n] (row-major, padded stride)
   if (a.ks == 1) {
     // the dense sum, then the outliers (row_fma, engine.cpp:111-122): their
     // per-row CSR sums (exact fp32, CSR order) come from the prologue kernel
@@ -420,28 +441,50 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     for (uint32_t i = threadIdx.x; i < kTileRows * a.batch; i += blockDim.x) {
       const uint32_t t = i % kTileRows, n = i / kTileRows, row = tile * kTileRows + t;
       if (row < G.rows)
-        a.y[(size_t)n * G.rows + row] = s_dense[t * 17 + n] + __ldg(a.ycsr + (size_t)n * G.rows + row);
+        a.y[(size_t)n * G.rows + row] = s_dense[t * kDenseStride + n] + __ldg(a.ycsr + (size_t)n * G.rows + row);
     }
   } else {
     // split-K: the tile's K splits form one thread-block cluster; CTA `split`
     // sums rows [split * 128 / ks, ...) over the splits' shared-memory
     // partials (distributed shared memory) in split order -- deterministic
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (threadIdx.x == 0) gstamp(a, 3);  // cluster joined
     pdl_wait();
+    if (threadIdx.x == 0) gstamp(a, 4);  // prologue kernel complete
     const uint32_t r0 = split * kTileRows / a.ks, r1 = (split + 1) * kTileRows / a.ks;
     const uint32_t local = smem_addr(s_dense);
-    for (uint32_t i = threadIdx.x; i < (r1 - r0) * a.batch; i += blockDim.x) {
-      const uint32_t t = r0 + i % (r1 - r0), n = i / (r1 - r0), row = tile * kTileRows + t;
-      float s = 0.0f;
-      for (uint32_t sp = 0; sp < a.ks; ++sp) {
-        uint32_t remote;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + (t * 17 + n) * 4), "r"(sp));
-        float v;
-        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote));
-        s += v;
+    // item = (row, 4 columns): the splits' float4 partials all in flight, then
+    // summed in split order
+    const uint32_t nr = r1 - r0, nc4 = (a.batch + 3) / 4;
+    for (uint32_t i = threadIdx.x; i < nr * nc4; i += blockDim.x) {
+      const uint32_t t = r0 + i % nr, c4 = i / nr, row = tile * kTileRows + t;
+      float4 v[8];
+#pragma unroll
+      for (uint32_t sp = 0; sp < 8; ++sp) {
+        v[sp] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (sp < a.ks) {
+          uint32_t remote;
+          asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + (t * kDenseStride + 4 * c4) * 4), "r"(sp));
+          asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(v[sp].x), "=f"(v[sp].y), "=f"(v[sp].z), "=f"(v[sp].w)
+                       : "r"(remote)
+                       : "memory");
+        }
       }
-      if (row < G.rows) a.y[(size_t)n * G.rows + row] = s + __ldg(a.ycsr + (size_t)n * G.rows + row);
+      float4 sum = v[0];
+#pragma unroll
+      for (uint32_t sp = 1; sp < 8; ++sp)
+        if (sp < a.ks) sum.x += v[sp].x, sum.y += v[sp].y, sum.z += v[sp].z, sum.w += v[sp].w;
+      if (row < G.rows) {
+        const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+          const uint32_t n = 4 * c4 + k;
+          if (n < a.batch) a.y[(size_t)n * G.rows + row] = sv[k] + __ldg(a.ycsr + (size_t)n * G.rows + row);
+        }
+      }
     }
+    if (threadIdx.x == 0) gstamp(a, 5);  // partials summed (thread 0)
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
   if (threadIdx.x == 0) gstamp(a, 6);  // y stored
@@ -451,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 }
 
 constexpr size_t kGemmSmem = 1024 + kABufs * kATileBytes + kBSlots * kBStageBytes + kWSlots * kWStageBytes + 512 +
-                             kTileRows * 17 * 4;
+                             kTileRows * kDenseStride * 4 + 16;
 static_assert(kGemmSmem <= 227 * 1024, "gemm shared memory");
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -570,7 +613,8 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  static const bool no_pdl = std::getenv("QW_GEMM_NOPDL") != nullptr;  // diagnostics
+  cfg.numAttrs = no_pdl ? 1 : 2;
   void* params[] = {&a};
   return (int)cudaLaunchKernelExC(&cfg, (const void*)gemm_kernel, params);
 }

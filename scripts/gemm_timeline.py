@@ -20,7 +20,7 @@ for _ in range(3):
 a = st.cpu().numpy().reshape(512, 8)
 a = a[a[:, 0] > 0]
 t0 = a[:, 0].min()
-names = ["setup", "s3 W present", "s3 decoded", "s3 A free", "s3 A published", "s3 MMA sees A", "y stored", "acc ready"]
+names = ["setup", "s3 W present", "CTA joined", "cluster joined", "prologue done", "sums done (t0)", "y stored", "acc ready"]
 print(f"{rows}x{cols} b={b}: {a.shape[0]} CTAs")
 for i, nm in enumerate(names):
     v = a[:, i]
