@@ -828,7 +828,7 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   const size_t unit_bytes = (size_t)p.uq * G.dense_bytes;
   const size_t units = (p.nq_max + p.uq - 1) / p.uq;
   // long ranges (group launches, big layers): two teams, the whole SM
-  p.teams = (!p.wide && p.nq_max >= env_u32("QW_TEAMS_MIN_NQ", 12) && p.kmax <= 2 && p.uniform_rb && p.xsm &&
+  p.teams = (!p.wide && p.nq_max >= env_u32("QW_TEAMS_MIN_NQ", 4) && p.kmax <= 2 && p.uniform_rb && p.xsm &&
              p.uq == 2) ? 2 : 1;
   const size_t half_sm = (p.teams == 2 || p.wide ? 200 : env_u32("QW_SMEM_KB", 112)) * 1024, full_sm = 220 * 1024;
   size_t S = units;
