@@ -100,14 +100,15 @@ __device__ __forceinline__ float p2(int e) { return __uint_as_float((uint32_t)(m
 // holds 2-bit permuted channels [96 st, 96 st + 96) then 4-bit channels
 // n2p + [32 st, 32 st + 32); element (k, n) of a stage at
 // (k % 8) * 2 + (n % 8) * 16 + (n / 8) * 128 + (k / 8) * 256.
-// Grid (chunks, 16): every CTA re-derives its column's power-of-two scale
-// from a full (L2-resident, independent-load) max, then converts one
-// element per thread, so no thread waits on a chain of dependent loads.
-constexpr uint32_t kPrepThreads = 256;
+// Grid (chunks + csr_blocks, 16): a chunk CTA re-derives its column's
+// power-of-two scale from a full (L2-resident, independent-load) max, then
+// converts kPrepPer elements per thread (independent loads, so no thread waits
+// on a chain); few enough CTAs to run in one wave beside the GEMM's.
+constexpr uint32_t kPrepThreads = 256, kPrepPer = 4;
 // CSR outliers of every row for all columns: y_csr[n][r] = sum over the row's
 // entries, in CSR order, of fp16(v) * x_n[perm[col]] (sparse_matvec,
-// outliers.cpp:131-141), exact fp32.  One thread per row; the row's entries
-// are loaded first so the x gathers of the columns are independent.
+// outliers.cpp:131-141), exact fp32.  One thread per (row, column); the row's
+// entries are loaded first so the x gathers are independent.
 __device__ __forceinline__ void csr_row(const float* __restrict__ xn, const uint16_t* __restrict__ perm,
                                         const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ csr,
                                         uint32_t rows, float* __restrict__ yn, uint32_t row) {
@@ -164,18 +165,19 @@ __global__ void __launch_bounds__(kPrepThreads) xprep_kernel(const float* __rest
   const int e = (eb == 0 ? -126 : eb - 127) - 14;  // max |x'| in [2^14, 2^15)
   if (threadIdx.x == 0 && blockIdx.x == 0) xexp[n] = e;
   const uint32_t n2 = G.cols - G.n4;
-  const uint32_t i = blockIdx.x * kPrepThreads + threadIdx.x;
-  if (i >= stages * kStageK) return;
-  (void)n2;
-  const uint32_t st = i / kStageK, k = i % kStageK;
-  const uint32_t slot = k < 96 ? 96 * st + k : G.n2p + 32 * st + (k - 96);
-  float v = 0.0f;
-  if (n < batch && !(slot >= n2 && slot < G.n2p)) {
-    const int a = max(-126, min(127, -e));
-    v = __ldg(xn + perm[slot]) * p2(a) * p2(-e - a);
+  const int ea = max(-126, min(127, -e));
+  const float f1 = p2(ea), f2 = p2(-e - ea);
+#pragma unroll
+  for (uint32_t u = 0; u < kPrepPer; ++u) {
+    const uint32_t i = (blockIdx.x * kPrepPer + u) * kPrepThreads + threadIdx.x;
+    if (i >= stages * kStageK) break;
+    const uint32_t st = i / kStageK, k = i % kStageK;
+    const uint32_t slot = k < 96 ? 96 * st + k : G.n2p + 32 * st + (k - 96);
+    float v = 0.0f;
+    if (n < batch && !(slot >= n2 && slot < G.n2p)) v = __ldg(xn + perm[slot]) * f1 * f2;
+    const uint32_t off = (k % 8) * 2 + (n % 8) * 16 + (n / 8) * 128 + (k / 8) * 256;
+    xpt[(size_t)st * (kBStageBytes / 2) + off / 2] = __half_as_ushort(__float2half_rn(v));
   }
-  const uint32_t off = (k % 8) * 2 + (n % 8) * 16 + (n / 8) * 128 + (k / 8) * 256;
-  xpt[(size_t)st * (kBStageBytes / 2) + off / 2] = __half_as_ushort(__float2half_rn(v));
 }
 
 // ---------------------------------------------------------------- GEMM
@@ -583,7 +585,7 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   const Geometry& G = L.g;
   const GemmPlan& p = L.gemm;
   cudaStream_t st = (cudaStream_t)stream;
-  const uint32_t chunks = (p.stages * kStageK + kPrepThreads - 1) / kPrepThreads;
+  const uint32_t chunks = (p.stages * kStageK + kPrepThreads * kPrepPer - 1) / (kPrepThreads * kPrepPer);
   const uint32_t csr_blocks = (G.rows + kPrepThreads - 1) / kPrepThreads;
   xprep_kernel<<<dim3(chunks + csr_blocks, 16), kPrepThreads, 0, st>>>(x, L.perm16, G, p.stages, batch, p.xpt,
                                                                        p.xexp, chunks, L.row_ptr, L.csr, p.ycsr);

@@ -1,4 +1,8 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --no-cpu > gpurun_out/bench.json 2> gpurun_out/bench.err
-python -c "import json;d=json.load(open('gpurun_out/bench.json'));print(d['value'],d['independent']['value'],d['chain_kernel']['value'],d['roofline'])"
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "batch" 2>&1 | tail -2
+timeout 600 python scripts/batch_sweep.py > gpurun_out/batch_sweep.jsonl 2> gpurun_out/batch_sweep.err
+python - <<'P'
+import json
+for l in open("gpurun_out/batch_sweep.jsonl"):
+    d = json.loads(l); print(d["shape"], d["batch"], d["us_per_call"], d["gb_s"])
+P
