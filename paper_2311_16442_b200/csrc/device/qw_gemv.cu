@@ -181,6 +181,7 @@ struct GemvArgs {
   uint32_t repeat;  // diagnostics: consumers re-run the resident quads this many times
   uint32_t wait_x;  // x is the previous kernel's output: griddepcontrol.wait before reading it
   uint32_t pre;     // precompute 1st-order scales of resident units before x
+  uint32_t npre_max;  // at most this many units precomputed
   uint32_t x_first; // stage x before the scale precompute (no predecessor overlap)
   uint32_t so_off, part_off, csr_off, x_off, win_off, pre_off, bar_off;
   const uint8_t* pf_ptr[GemvPlan::kMaxPf];  // next launch's weights -> L2 (a slice per CTA)
@@ -387,7 +388,9 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
   }
   float* win = reinterpret_cast<float*>(smem + a.win_off) + warp * kWinWords;
   const uint32_t reps = (a.repeat > 1 && nunit <= S) ? a.repeat : 1;
-  const uint32_t npre = a.pre ? min(nunit, S) : 0u;  // units resident before x: scales precomputed
+  // units whose scales are precomputed before x (they must have landed first:
+  // capped so the main loop can start under the rest of the weight stream)
+  const uint32_t npre = a.pre ? min(min(nunit, S), a.npre_max) : 0u;
 
   // One consumer body per group type (warp-uniform), per-lane constants hoisted.
   auto run = [&](auto two_tag) {
@@ -918,7 +921,10 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   a.dbg_global = global_clock;
   a.wait_x = (flags & kXIndependent) ? 0u : 1u;
   a.pre = 1;
-  a.x_first = env_u32("QW_XFIRST", 0);
+  // default: no precompute for team kernels (they start after their predecessor: the main
+  // loop must run under the weight stream), all resident units otherwise (PDL overlap)
+  a.npre_max = env_u32("QW_NPRE_MAX", p.teams == 2 ? 0u : 1000000u);
+  a.x_first = env_u32("QW_XFIRST", p.teams == 2 ? 1u : 0u);
   if (const char* e = std::getenv("QW_NO_PRE")) a.pre = std::atoi(e) ? 0u : 1u;
   a.repeat = repeat;
   std::copy(p.cta_seg, p.cta_seg + p.grid, a.cta_seg);

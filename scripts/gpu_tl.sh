@@ -1,8 +1,5 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "batch" 2>&1 | tail -2
-timeout 600 python scripts/batch_sweep.py > gpurun_out/batch_sweep.jsonl 2> gpurun_out/batch_sweep.err
-python - <<'P'
-import json
-for l in open("gpurun_out/batch_sweep.jsonl"):
-    d = json.loads(l); print(d["shape"], d["batch"], d["us_per_call"], d["gb_s"])
-P
+for v in "QW_NPRE_MAX=1000000" "QW_NPRE_MAX=0" "QW_NPRE_MAX=2" "QW_NPRE_MAX=4" "QW_NPRE_MAX=2 QW_XFIRST=1" "QW_NPRE_MAX=0 QW_XFIRST=1"; do
+  env $v timeout 600 python bench.py --no-cpu --steps 10 > gpurun_out/b.json 2> gpurun_out/b.err
+  echo "$v: $(python -c "import json;d=json.load(open('gpurun_out/b.json'));print(d['value'],d['independent']['value'],d['roofline']['achieved'])" 2>&1 | tail -1)"
+done
