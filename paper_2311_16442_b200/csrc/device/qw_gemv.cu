@@ -539,6 +539,13 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
       if (a.wait_x) pdl_wait();  // x is the previous kernel's output
       xs = a.x;
     }
+    // Two teams need the same X: team 0 prepares it and hands it to team 1
+    // through team 1's (not yet used) reduction windows.
+    half2 X[KG][16], nsxh[KG];
+    float yscale;
+    const bool share = TM && KG == 1 && T == 2;
+    uint32_t* xsh = reinterpret_cast<uint32_t*>(smem + a.win_off) + (W + wt) * kWinWords + lane * 20u;
+    if (!share || team == 0) {
     const uint32_t n2 = G.cols - G.n4;
     float xv[KG][16];
     float mx = 0.0f;
@@ -576,7 +583,6 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
       const int e1 = max(-126, min(127, e));
       f1[bi] = pow2f(e1), f2[bi] = pow2f(max(-126, min(127, e - e1)));
     }
-    half2 X[KG][16], nsxh[KG];
 #pragma unroll
     for (int k = 0; k < KG; ++k) {
       const uint32_t g = gk[k];
@@ -598,7 +604,31 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
       nsxh[k] = __float2half2_rn(-sx * pow2f(-zp));
     }
     // every accumulated term is in units of 2^(sh + 24) (and 2^P for 2-bit s1)
-    const float yscale = pow2f(max(-126, min(127, sh + 24))) * (TWO ? 1.0f / s_scale : 1.0f);
+    yscale = pow2f(max(-126, min(127, sh + 24))) * (TWO ? 1.0f / s_scale : 1.0f);
+    if (share) {
+      uint4* d = reinterpret_cast<uint4*>(xsh);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        d[q] = make_uint4(*reinterpret_cast<uint32_t*>(&X[0][4 * q]), *reinterpret_cast<uint32_t*>(&X[0][4 * q + 1]),
+                          *reinterpret_cast<uint32_t*>(&X[0][4 * q + 2]), *reinterpret_cast<uint32_t*>(&X[0][4 * q + 3]));
+      d[4] = make_uint4(*reinterpret_cast<uint32_t*>(&nsxh[0]), __float_as_uint(yscale), 0u, 0u);
+    }
+    }
+    if (share) {
+      named_sync(3, 2 * W * 32);
+      if (team == 1) {
+        const uint4* d = reinterpret_cast<const uint4*>(xsh);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 v = d[q];
+          X[0][4 * q] = as_h2(v.x), X[0][4 * q + 1] = as_h2(v.y), X[0][4 * q + 2] = as_h2(v.z),
+          X[0][4 * q + 3] = as_h2(v.w);
+        }
+        const uint4 v = d[4];
+        nsxh[0] = as_h2(v.x), yscale = __uint_as_float(v.y);
+        __syncwarp();  // every lane has read before the window is reused
+      }
+    }
     if (threadIdx.x == 0) stamp(a.dbg, 2);  // prologue done
     if (threadIdx.x == 0 && a.dbg && nunit) {  // diagnostics: the first unit is in
       mbar_wait(&s_full[0], 0);
