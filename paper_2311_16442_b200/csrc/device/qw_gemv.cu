@@ -182,6 +182,7 @@ struct GemvArgs {
   uint32_t wait_x;  // x is the previous kernel's output: griddepcontrol.wait before reading it
   uint32_t pre;     // precompute 1st-order scales of resident units before x
   uint32_t npre_max;  // at most this many units precomputed
+  uint32_t x_gate;    // the producer issues this many units, then waits for x
   uint32_t x_first; // stage x before the scale precompute (no predecessor overlap)
   uint32_t so_off, part_off, csr_off, x_off, win_off, pre_off, bar_off;
   const uint8_t* pf_ptr[GemvPlan::kMaxPf];  // next launch's weights -> L2 (a slice per CTA)
@@ -300,9 +301,14 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
           pf_pos += n, pf_done += n;
         }
       };
+      // never gate below the units the consumers precompute before x (deadlock)
+      const uint32_t x_gate = max(a.x_gate, a.pre ? min(min(nunit, S), a.npre_max) : 0u);
       uint32_t slot = 0, phase = 0;
       for (uint32_t u = 0; u < nunit; ++u) {
         const uint32_t bytes = min((uint32_t)NQ, nq - NQ * u) * dense;
+        // after the first units, hold the stream until x is staged: x then
+        // is not queued behind this SM's whole weight range
+        if (XSM && u == x_gate) mbar_wait(s_xbar, 0);
         if (u >= S) mbar_wait(&s_empty[slot], phase ^ 1u);
         mbar_expect_tx(&s_full[slot], bytes);
         bulk_load_nohint(smem + (size_t)slot * NQ * dense, src, bytes, &s_full[slot]);
@@ -490,7 +496,16 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
 #pragma unroll
         for (int j = 0; j < kXr; ++j)
           if (tid + j * nth < n4) sx4[tid + j * nth] = xr[j];
-        for (uint32_t i = tid + kXr * nth; i < n4; i += nth) sx4[i] = __ldg(gx + i);
+        // the rest (wide layers): 4 loads in flight per batch
+        for (uint32_t i = tid + kXr * nth; i < n4; i += 4 * nth) {
+          float4 v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (i + j * nth < n4) v[j] = __ldg(gx + i + j * nth);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (i + j * nth < n4) sx4[i + j * nth] = v[j];
+        }
       } else {
         for (uint32_t i = tid; i < G.cols; i += nth) s_x[i] = __ldg(a.x + i);
       }
@@ -953,8 +968,10 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   a.pre = 1;
   // default: no precompute for team kernels (they start after their predecessor: the main
   // loop must run under the weight stream), all resident units otherwise (PDL overlap)
-  a.npre_max = env_u32("QW_NPRE_MAX", p.teams == 2 ? 0u : 1000000u);
-  a.x_first = env_u32("QW_XFIRST", p.teams == 2 ? 1u : 0u);
+  a.npre_max = env_u32("QW_NPRE_MAX", (p.teams == 2 || p.wide) ? 0u : 1000000u);
+  const bool alone = p.teams == 2 || p.wide;  // one CTA per SM: starts after its predecessor
+  a.x_first = env_u32("QW_XFIRST", alone ? 1u : 0u);
+  a.x_gate = env_u32("QW_XGATE", alone ? 4u : 1000000u);
   if (const char* e = std::getenv("QW_NO_PRE")) a.pre = std::atoi(e) ? 0u : 1u;
   a.repeat = repeat;
   std::copy(p.cta_seg, p.cta_seg + p.grid, a.cta_seg);
