@@ -50,6 +50,7 @@ struct GemvPlan {
   float s_scale = 1.0f;  // 2^-P applied to 2-bit s1 so 15 * max scale2 * 2^-P fits fp16
   uint32_t so_off = 0, part_off = 0, xg_off = 0, misc_off = 0, win_off = 0, pre_off = 0, bar_off = 0;  // smem layout
   uint32_t smem = 0;
+  uint32_t pre = 1, npre_max = 0, x_first = 0, x_gate = 0, pf_late = 1;  // launch policy (plan_ctas)
   // decode chains: the next launch's packed weights (quad records, 2-order
   // rows), streamed into L2 by this launch's CTAs (one slice each) so HBM
   // keeps streaming while the SMs are still busy with this launch

@@ -895,6 +895,18 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   p.pre_off = p.win_off + (uint32_t)win_bytes;
   p.bar_off = (uint32_t)align_up(p.pre_off + pre_bytes(S), 8);
   p.smem = (uint32_t)(p.bar_off + (2 * S + 2) * 8);
+  // launch policy (fixed at plan time; the env knobs are diagnostics).  A CTA
+  // that owns its SM (teams / wide) starts after its predecessor: no scale
+  // precompute (the main loop must run under the weight stream), x first, and
+  // the producer holds the stream after 4 units until x is staged.  Otherwise
+  // (two CTAs per SM under PDL) the resident units' scales are precomputed
+  // while the predecessor still runs.
+  const bool alone = p.teams == 2 || p.wide;
+  p.pre = env_u32("QW_NO_PRE", 0) ? 0u : 1u;
+  p.npre_max = env_u32("QW_NPRE_MAX", alone ? 0u : 1000000u);
+  p.x_first = env_u32("QW_XFIRST", alone ? 1u : 0u);
+  p.x_gate = env_u32("QW_XGATE", alone ? 4u : 1000000u);
+  p.pf_late = env_u32("QW_PF_LATE", 1);
   static bool attr_set = false;  // raise the opt-in limit once per process
   if (!attr_set) {
     for (bool uni : {false, true})
@@ -959,20 +971,13 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   a.grid = p.grid, a.nq_max = p.nq_max, a.rb_magic = p.rb_magic, a.rb_one = p.rb_one;
   a.so_off = p.so_off, a.part_off = p.part_off, a.csr_off = p.misc_off, a.x_off = p.xg_off, a.win_off = p.win_off, a.pre_off = p.pre_off;
   a.bar_off = p.bar_off;
-  a.pf_n = env_u32("QW_NO_PF", 0) ? 0u : p.pf_n;
-  a.pf_late = env_u32("QW_PF_LATE", 1);
+  a.pf_n = p.pf_n;
+  a.pf_late = p.pf_late;
   for (uint32_t r = 0; r < GemvPlan::kMaxPf; ++r) a.pf_ptr[r] = p.pf_ptr[r], a.pf_bytes[r] = p.pf_bytes[r];
   a.dbg = dbg;
   a.dbg_global = global_clock;
   a.wait_x = (flags & kXIndependent) ? 0u : 1u;
-  a.pre = 1;
-  // default: no precompute for team kernels (they start after their predecessor: the main
-  // loop must run under the weight stream), all resident units otherwise (PDL overlap)
-  a.npre_max = env_u32("QW_NPRE_MAX", (p.teams == 2 || p.wide) ? 0u : 1000000u);
-  const bool alone = p.teams == 2 || p.wide;  // one CTA per SM: starts after its predecessor
-  a.x_first = env_u32("QW_XFIRST", alone ? 1u : 0u);
-  a.x_gate = env_u32("QW_XGATE", alone ? 4u : 1000000u);
-  if (const char* e = std::getenv("QW_NO_PRE")) a.pre = std::atoi(e) ? 0u : 1u;
+  a.pre = p.pre, a.npre_max = p.npre_max, a.x_first = p.x_first, a.x_gate = p.x_gate;
   a.repeat = repeat;
   std::copy(p.cta_seg, p.cta_seg + p.grid, a.cta_seg);
   std::copy(p.cta_q0, p.cta_q0 + p.grid, a.cta_q0);
