@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
         }
       };
       // never gate below the units the consumers precompute before x (deadlock)
-      const uint32_t x_gate = max(a.x_gate, a.pre ? min(min(nunit, S), a.npre_max) : 0u);
+      const uint32_t x_gate = max(a.x_gate, (!TM && a.pre) ? min(min(nunit, S), a.npre_max) : 0u);
       uint32_t slot = 0, phase = 0;
       for (uint32_t u = 0; u < nunit; ++u) {
         const uint32_t bytes = min((uint32_t)NQ, nq - NQ * u) * dense;
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
   const uint32_t reps = (a.repeat > 1 && nunit <= S) ? a.repeat : 1;
   // units whose scales are precomputed before x (they must have landed first:
   // capped so the main loop can start under the rest of the weight stream)
-  const uint32_t npre = a.pre ? min(min(nunit, S), a.npre_max) : 0u;
+  const uint32_t npre = (!TM && a.pre) ? min(min(nunit, S), a.npre_max) : 0u;  // team kernels: never (policy)
 
   // One consumer body per group type (warp-uniform), per-lane constants hoisted.
   auto run = [&](auto two_tag) {
