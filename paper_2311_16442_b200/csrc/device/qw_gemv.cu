@@ -870,7 +870,7 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   const size_t fixed = align_up(so_bytes, 16) + part_bytes + align_up(misc_bytes, 16) + x_bytes +
                        win_bytes + 64;
   // precomputed 1st-order scales: one uint2 per (slot, quad, k, lane)
-  auto pre_bytes = [&](size_t s) { return s * p.uq * p.kmax * p.warps * 32 * 8; };
+  auto pre_bytes = [&](size_t s) { return p.teams == 2 ? (size_t)0 : s * p.uq * p.kmax * p.warps * 32 * 8; };
   // ring: the CTA's whole quad range when it fits in ~half an SM (so the next
   // layer's CTA fits beside it under PDL), else as many slots as fit
   const size_t unit_bytes = (size_t)p.uq * G.dense_bytes;
@@ -885,7 +885,13 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   };
   while (S > 3 && total_b(S) > half_sm) --S;
   while (S > 2 && total_b(S) > full_sm) --S;
-  if (total_b(S) > full_sm) return (int)cudaErrorInvalidConfiguration;
+  // two teams share a ring: with an even slot count slot s only ever holds
+  // team (s % 2)'s units, so a team's successive units in a slot are
+  // successive barrier phases.  (With an odd count a fast team could wait for
+  // phase p + 2 of a slot while the other team's phase p + 1 is still in
+  // flight, and the parity wait would alias with the completed phase p.)
+  if (p.teams == 2 && S < units && (S & 1)) --S;
+  if (total_b(S) > full_sm || (p.teams == 2 && S < 2)) return (int)cudaErrorInvalidConfiguration;
   p.nslot = (uint32_t)S;
   p.so_off = (uint32_t)align_up(S * unit_bytes, 128);
   p.part_off = p.so_off + (uint32_t)align_up(so_bytes, 16);
@@ -1085,8 +1091,8 @@ __device__ __forceinline__ void chain_consume(const ChainStep& st, const ChainCt
   const uint32_t W = st.W, W2 = st.W2, W4 = W - W2, T = st.T, team = c.team, wt = c.wt;
   const uint32_t dense = G.dense_bytes, nunit = c.nunit;
   if (team >= T) return;  // idle warp this step (W does not divide 16)
-  // the team's units u = team, team + T, ...: ring position gu + u
-  uint32_t slot = (c.gu + team) % c.S, phase = ((c.gu + team) / c.S) & 1u;
+  // ring position of the step's first unit
+  uint32_t slot = c.gu % c.S, phase = (c.gu / c.S) & 1u;
   const uint32_t arrive_count = kChainEmpty / W;
   const uint32_t rb_magic = st.rb_magic, rb_one = st.rb_one;
   auto row_block = [&](uint32_t r) { return rb_one ? r : __umulhi(r, rb_magic); };
@@ -1243,9 +1249,16 @@ __device__ __forceinline__ void chain_consume(const ChainStep& st, const ChainCt
       }
     }
 
-    uint32_t wrow = 0, ufirst = 0;
-    for (uint32_t u = team; u < nunit; u += T) {
+    uint32_t wrow = 0, ufirst = 0, owner = 0;
+    for (uint32_t u = 0; u < nunit; ++u, owner = owner + 1 == T ? 0 : owner + 1) {
+      // every unit's phase is observed in order (a parity wait that skipped a
+      // phase could alias with an older completed one); only the team's own
+      // units (u = team mod T) are decoded
       mbar_wait(&c.full[slot], phase);
+      if (owner != team) {
+        if (++slot == c.S) slot = 0, phase ^= 1u;
+        continue;
+      }
       const uint8_t* sb = c.ring + (size_t)slot * c.slot_bytes;
       float acc[NQ][4];
 #pragma unroll
@@ -1297,7 +1310,7 @@ __device__ __forceinline__ void chain_consume(const ChainStep& st, const ChainCt
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_cnt(&c.empty[slot], arrive_count);
-      for (slot += T; slot >= c.S;) slot -= c.S, phase ^= 1u;
+      if (++slot == c.S) slot = 0, phase ^= 1u;
 #pragma unroll
       for (int j = 0; j < NQ; ++j)
         *reinterpret_cast<float4*>(win + win_base(lane) + wrow + 4 * j) =

@@ -336,3 +336,19 @@ def test_decode_chain_rejects_unsupported_geometry():
     with pytest.raises(qw.QWeightError) as ei:
         qw.DecodeChain([([d], x, [y], False)])
     assert ei.value.status == 5
+
+
+def test_team_ring_is_race_free():
+    """Two teams sharing a slot ring (8192-wide: 25 KB units, a handful of
+    slots, 7 units per CTA): every run equals the first and the f64 oracle
+    (an odd slot count once let a fast team alias a parity phase)."""
+    torch = _torch()
+    layer = qw.synth_layer(8192, 8192, seed=7)
+    dls = [qw.DeviceLayer(layer)]
+    dls.append(dls[0].clone())
+    x = torch.from_numpy(qw.synth_activation(8192, 8)).cuda()
+    first = dls[0].matvec(x).clone()
+    assert rel_l2(first.cpu().numpy(), oracle.matvec_f64(layer, x.cpu().numpy())) <= TOL
+    for _ in range(20):
+        for d in dls:
+            assert torch.equal(d.matvec(x, pdl=True), first)
