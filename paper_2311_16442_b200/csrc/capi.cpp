@@ -273,7 +273,10 @@ void repack(const qwb::PackedLayer& L, const qwdev::Geometry& g, std::vector<uin
     }
   csr.resize(L.csr.col_ind.size());
   for (size_t e = 0; e < csr.size(); ++e)
-    csr[e] = (uint32_t)L.csr.col_ind[e] | ((uint32_t)L.csr.values[e] << 16);
+    // the entry names the ORIGINAL channel of its permuted column (perm[col],
+    // a real channel: outliers live in the 2-bit non-pad region), so the
+    // kernels read x without a perm lookup
+    csr[e] = L.plan.perm[L.csr.col_ind[e]] | ((uint32_t)L.csr.values[e] << 16);
 }
 
 template <class T>

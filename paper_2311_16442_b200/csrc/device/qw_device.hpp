@@ -18,7 +18,8 @@
 //
 // sorder is kept per 2-order row block as u32 (scale2 | zero2 << 16) with
 // the row stride padded to 16 bytes.  Outliers are the reference CSR with
-// col/value fused into one u32 (col | fp16 << 16) next to the original
+// (original channel of the permuted col, fp16 value) fused into one u32
+// (channel | fp16 << 16) next to the original
 // row_ptr.
 #pragma once
 
@@ -95,7 +96,7 @@ struct DeviceLayer {
   uint32_t* perm = nullptr;      // padded_cols (0xFFFFFFFF = pad)
   uint16_t* perm16 = nullptr;    // padded_cols, original channel (pads: cols, a zero slot of the staged x)
   uint32_t* row_ptr = nullptr;   // rows + 1
-  uint32_t* csr = nullptr;       // nnz (col | fp16 << 16)
+  uint32_t* csr = nullptr;       // nnz (perm[col] | fp16 << 16): x channel + value
 };
 
 // Per-stream scratch (kept in the ABI for the batched path; the fused

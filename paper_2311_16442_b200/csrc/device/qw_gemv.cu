@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
         ent[j] = e < n ? __ldg(g_csr + e_lo + e) : 0u;
       }
 #pragma unroll
-      for (int j = 0; j < kPer; ++j) src[j] = __ldg(g_perm + (ent[j] & 0xFFFFu));
+      for (int j = 0; j < kPer; ++j) src[j] = ent[j] & 0xFFFFu;  // original channel (repack)
     };
     if (n) fetch(0);
     __syncwarp();
@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
       else if (a.wait_x)
         pdl_wait();
     }
+    uint32_t t0 = 0;
     for (uint32_t c0 = 0; c0 < n; c0 += 32u * kPer) {
       const uint32_t c1 = min(c0 + 32u * kPer, n);
 #pragma unroll
@@ -357,10 +358,17 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
       }
       __syncwarp();
       if (c1 < n) fetch(c1);
-      for (uint32_t t = lane; t < nrows; t += 32) {
+      // rows the chunk touches: [t0, ...) with rp[t0 + 1] > c0 (warp ballot advance)
+      for (;;) {
+        const uint32_t t = t0 + lane;
+        const uint32_t done = __ballot_sync(0xFFFFFFFFu, t < nrows && s_rp[t + 1] <= c0);
+        t0 += __popc(done);
+        if (done != 0xFFFFFFFFu) break;
+      }
+      for (uint32_t t = t0 + lane; t < nrows && s_rp[t] < c1; t += 32) {
         const uint32_t lo = max(s_rp[t], c0), hi = min(s_rp[t + 1], c1);
         float s = s_csr[t];
-        for (uint32_t e = lo; e < hi; ++e) s += s_prod[e - c0];
+        for (uint32_t e = lo; e < hi; ++e) s += s_prod[e - c0];  // CSR order within the row
         s_csr[t] = s;
       }
       __syncwarp();
@@ -1431,11 +1439,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
           ent[j] = e < n ? __ldg(g_csr + e_lo + e) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) src[j] = __ldg(g_perm + (ent[j] & 0xFFFFu));
+        for (int j = 0; j < kPer; ++j) src[j] = ent[j] & 0xFFFFu;  // original channel (repack)
       };
       if (n) fetch(0);
       __syncwarp();
       mbar_wait(xbar, s & 1u);  // x of step s staged
+      uint32_t t0 = 0;
       for (uint32_t c0 = 0; c0 < n; c0 += 32u * kPer) {
         const uint32_t c1 = min(c0 + 32u * kPer, n);
 #pragma unroll
@@ -1445,7 +1454,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
         }
         __syncwarp();
         if (c1 < n) fetch(c1);
-        for (uint32_t t = lane; t < nrows; t += 32) {
+        for (;;) {  // rows the chunk touches: [t0, ...)
+          const uint32_t t = t0 + lane;
+          const uint32_t done = __ballot_sync(0xFFFFFFFFu, t < nrows && s_rp[t + 1] <= c0);
+          t0 += __popc(done);
+          if (done != 0xFFFFFFFFu) break;
+        }
+        for (uint32_t t = t0 + lane; t < nrows && s_rp[t] < c1; t += 32) {
           const uint32_t lo = max(s_rp[t], c0), hi = min(s_rp[t + 1], c1);
           float acc = s_csr[t];
           for (uint32_t e = lo; e < hi; ++e) acc += s_prod[e - c0];

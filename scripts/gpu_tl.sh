@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-echo default; python scripts/_dbg_chain.py 28672 8192 6 20 2>&1 | tail -1
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; grep -E "passed|failed" gpurun_out/pytest_gpu.log | tail -1
 timeout 600 python bench.py --no-cpu --steps 10 > gpurun_out/b.json 2> gpurun_out/b.err
 python -c "import json;d=json.load(open('gpurun_out/b.json'));print(d['value'],d['independent']['value'],d['chain_kernel']['value'],d['roofline']['achieved'])"
@@ -9,3 +8,4 @@ import json
 for l in open("gpurun_out/shape_sweep.jsonl"):
     d = json.loads(l); print(d["case"], d["us_per_call"], d["gb_s"], d["pct_of_hbm_peak"], "%.1e" % d["rel_l2_vs_f64"])
 P
+timeout 600 python scripts/batch_sweep.py > gpurun_out/batch_sweep.jsonl 2> gpurun_out/batch_sweep.err; tail -2 gpurun_out/batch_sweep.err
