@@ -218,6 +218,10 @@ typedef struct {
 int qw_chain_create(const qw_chain_step* steps, uint32_t n, qw_chain** out);
 int qw_chain_run(const qw_chain* chain, void* stream);
 int qw_chain_free(qw_chain* chain);
+/* Diagnostics: with QW_CHAIN_WATCH set at chain creation, a chain wait that
+ * spins for seconds records {code, arg, parity, cta, thread} per warp into
+ * host memory and traps; this copies those records out. */
+int qw_debug_chain_watch(uint32_t* out, uint32_t n);
 /* Host-buffer, synchronous, checked: length and finiteness as the reference
  * (engine.cpp:124-132).  x_len must equal batch * cols. */
 int qw_matvec_host(const qw_layer* layer, const float* x, uint64_t x_len,

@@ -95,6 +95,7 @@ _SIGS = {
     "qw_chain_create": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "qw_chain_run": (C.c_int, [C.c_void_p, C.c_void_p]),
     "qw_chain_free": (C.c_int, [C.c_void_p]),
+    "qw_debug_chain_watch": (C.c_int, [C.POINTER(C.c_uint32), C.c_uint32]),
     "qw_group_set_prefetch": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_uint32]),
     "qw_matvec_pdl": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
                                 C.c_void_p]),

@@ -521,6 +521,7 @@ int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
     std::vector<uint8_t> quads;
     std::vector<uint32_t> sorder, csr;
     repack(L, H->dev.g, quads, sorder, csr);
+    csr.resize(csr.size() + 4, 0u);  // padding: 16-byte aligned bulk copies of a CTA's entries may overrun
     std::vector<uint16_t> perm16(L.plan.perm.size());
     for (size_t i = 0; i < perm16.size(); ++i)
       perm16[i] = L.plan.perm[i] == qwb::kPad ? (uint16_t)L.cfg.cols : (uint16_t)L.plan.perm[i];  // pads: x[cols] = 0 slot
@@ -697,7 +698,7 @@ int qw_layer_clone(const qw_layer* L, qw_layer** out) {
       (e = dup(&H->dev.sorder, L->dev.sorder, (size_t)g.row_blocks * g.G2s * 4)) != cudaSuccess ||
       (e = dup(&H->dev.perm, L->dev.perm, (size_t)g.padded_cols * 4)) != cudaSuccess ||
       (e = dup(&H->dev.row_ptr, L->dev.row_ptr, ((size_t)g.rows + 1) * 4)) != cudaSuccess ||
-      (e = dup(&H->dev.csr, L->dev.csr, (size_t)g.nnz * 4)) != cudaSuccess ||
+      (e = dup(&H->dev.csr, L->dev.csr, ((size_t)g.nnz + 4) * 4)) != cudaSuccess ||
       (e = dup(&H->dev.perm16, L->dev.perm16, (size_t)g.padded_cols * 2)) != cudaSuccess) {
     free_dev(H->dev);
     return cuda_fail(e, "clone");
@@ -838,6 +839,13 @@ int qw_chain_run(const qw_chain* c, void* stream) {
   if (dev_now != c->device) cudaSetDevice(c->device);
   const int e = qwdev::launch_chain(c->plan, stream);
   return e ? cuda_fail((cudaError_t)e, "chain launch") : QW_OK;
+}
+
+int qw_debug_chain_watch(uint32_t* out, uint32_t n) {
+  const unsigned* w = qwdev::chain_watch();
+  if (!w || !out) return fail(QW_ERR_ARG, "chain watch: not enabled (QW_CHAIN_WATCH)");
+  std::memcpy(out, w, (size_t)std::min<uint32_t>(n, 148 * 32 * 8 * 4) * 4);
+  return QW_OK;
 }
 
 int qw_chain_free(qw_chain* c) {

@@ -50,6 +50,7 @@ struct GemvPlan {
   uint32_t nchunks = 0, nq_max = 0, uniform_rb = 0, xsm = 0, rb_magic = 0, rb_one = 0;
   float s_scale = 1.0f;  // 2^-P applied to 2-bit s1 so 15 * max scale2 * 2^-P fits fp16
   uint32_t so_off = 0, part_off = 0, xg_off = 0, misc_off = 0, win_off = 0, pre_off = 0, bar_off = 0;  // smem layout
+  uint32_t ent_off = 0, csr_stage = 0;  // CSR entries staged in shared memory (when they fit)
   uint32_t smem = 0;
   uint32_t pre = 1, npre_max = 0, x_first = 0, x_gate = 0, pf_late = 1;  // launch policy (plan_ctas)
   // decode chains: the next launch's packed weights (quad records, 2-order
@@ -156,5 +157,6 @@ struct ChainPlan;
 int plan_chain(ChainPlan** out, const ChainStepDesc* steps, uint32_t n, int num_sms);
 int launch_chain(const ChainPlan* p, void* stream);
 void free_chain(ChainPlan* p);
+const unsigned* chain_watch();  // diagnostics (QW_CHAIN_WATCH): [cta][warp][8] hang records, host memory
 
 }  // namespace qwdev

@@ -120,11 +120,11 @@ __device__ __forceinline__ void csr_row(const float* __restrict__ xn, const uint
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const uint32_t ent = e + u < e1 ? __ldg(csr + e + u) : 0u;
-      p[u] = half_bits_to_float(ent >> 16) * __ldg(xn + (ent & 0xFFFFu));  // original channel (repack)
+      p[u] = __fmul_rn(half_bits_to_float(ent >> 16), __ldg(xn + (ent & 0xFFFFu)));  // original channel (repack)
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (e + u < e1) acc += p[u];
+      if (e + u < e1) acc = __fadd_rn(acc, p[u]);
   }
   yn[row] = acc;
 }

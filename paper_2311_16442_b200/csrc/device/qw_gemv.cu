@@ -40,6 +40,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <cstdint>
 #include <type_traits>
 #include <vector>
@@ -185,6 +186,7 @@ struct GemvArgs {
   uint32_t x_gate;    // the producer issues this many units, then waits for x
   uint32_t x_first; // stage x before the scale precompute (no predecessor overlap)
   uint32_t so_off, part_off, csr_off, x_off, win_off, pre_off, bar_off;
+  uint32_t ent_off, csr_stage;  // the CTA's CSR entries staged in shared memory by one bulk copy
   const uint8_t* pf_ptr[GemvPlan::kMaxPf];  // next launch's weights -> L2 (a slice per CTA)
   uint32_t pf_bytes[GemvPlan::kMaxPf], pf_n, pf_late;
   unsigned long long* dbg;  // optional timeline: kTimelineEvents stamps per CTA
@@ -238,6 +240,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
   uint64_t* s_empty = s_full + S;
   uint64_t* s_sobar = s_empty + S;
   uint64_t* s_xbar = s_sobar + 1;
+  uint64_t* s_cbar = s_xbar + 1;
 
   const uint32_t seg = a.cta_seg[blockIdx.x];
   const uint32_t q0 = a.cta_q0[blockIdx.x], q1 = a.cta_q1[blockIdx.x];
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     mbar_init(&s_full[threadIdx.x], 1);
     mbar_init(&s_empty[threadIdx.x], W);  // one team consumes a unit
   }
-  if (threadIdx.x == 32) mbar_init(s_sobar, 1), mbar_init(s_xbar, NC);
+  if (threadIdx.x == 32) mbar_init(s_sobar, 1), mbar_init(s_xbar, NC), mbar_init(s_cbar, 1);
   if (XSM && threadIdx.x == 64) s_x[G.cols] = 0.0f;  // pads gather this zero (perm16 = cols)
   if (threadIdx.x == 0) stamp(a.dbg, 0);  // entry
   mbar_fence_init();
@@ -277,6 +280,16 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
         bulk_load_nohint(smem + a.so_off, g_sorder + (size_t)rb_first * G.G2s, so_bytes, s_sobar);
       } else {
         mbar_arrive(s_sobar);
+      }
+      if (a.csr_stage) {  // the CTA's outlier entries (x-independent): one bulk copy
+        const uint32_t e_lo = a.cta_e0[blockIdx.x], e_hi = a.cta_e1[blockIdx.x];
+        const uint32_t shift = e_lo & 3u, bytes = ((e_hi - e_lo + shift) * 4u + 15u) & ~15u;
+        if (e_hi > e_lo) {
+          mbar_expect_tx(s_cbar, bytes);
+          bulk_load_nohint(smem + a.ent_off, g_csr + (e_lo - shift), bytes, s_cbar);
+        } else {
+          mbar_arrive(s_cbar);
+        }
       }
       const uint8_t* src = g_quads + (size_t)q0 * dense;
       // L2 prefetch of this CTA's slice of the next launch's weights, issued
@@ -329,11 +342,45 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     const uint32_t n = e_hi - e_lo;
     constexpr int kPer = 8;
     uint32_t ent[kPer], src[kPer];
+    const uint32_t* s_ent = reinterpret_cast<const uint32_t*>(smem + a.ent_off) + (e_lo & 3u);
+    if (a.csr_stage) {
+      // entries staged by the producer: one row per lane, entries in CSR
+      // order, product then sum (outliers.cpp:131-141), no chunk barriers
+      __syncwarp();  // s_rp
+      if (n) {
+        mbar_wait(s_cbar, 0);
+        if (XSM) mbar_wait(s_xbar, 0);
+        else if (a.wait_x) pdl_wait();
+      }
+      for (uint32_t t = lane; t < nrows; t += 32) {
+        const uint32_t lo = s_rp[t], hi = s_rp[t + 1];
+        float acc = 0.0f;
+        uint32_t e = lo;
+        for (; e + 4 <= hi; e += 4) {  // loads of 4 entries in flight, sums in order
+          uint32_t w[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) w[j] = s_ent[e + j];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float xv = XSM ? s_x[w[j] & 0xFFFFu] : __ldg(a.x + (w[j] & 0xFFFFu));
+            acc = __fadd_rn(acc, __fmul_rn(half_bits_to_float(w[j] >> 16), xv));  // no contraction
+          }
+        }
+        for (; e < hi; ++e) {
+          const uint32_t w = s_ent[e];
+          acc = __fadd_rn(acc, __fmul_rn(half_bits_to_float(w >> 16), XSM ? s_x[w & 0xFFFFu] : __ldg(a.x + (w & 0xFFFFu))));
+        }
+        s_csr[t] = acc;
+      }
+      if (lane == 0) stamp(a.dbg, 6);  // outliers done
+      named_sync(2, (NC + 1) * 32);    // meet the consumers for the y store
+      return;
+    }
     auto fetch = [&](uint32_t c0) {
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
         const uint32_t e = c0 + lane + 32u * j;
-        ent[j] = e < n ? __ldg(g_csr + e_lo + e) : 0u;
+        ent[j] = e < n ? (a.csr_stage ? s_ent[e] : __ldg(g_csr + e_lo + e)) : 0u;
       }
 #pragma unroll
       for (int j = 0; j < kPer; ++j) src[j] = ent[j] & 0xFFFFu;  // original channel (repack)
@@ -855,7 +902,7 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   grid = std::max(grid, n);
   p.grid = grid;
   p.nq_max = 0;
-  uint32_t so_rows_max = 0, cta = 0;
+  uint32_t so_rows_max = 0, cta = 0, ent_max = 0;
   for (uint32_t l = 0; l < n; ++l) {
     const uint32_t g_l = grid * (l + 1) / n - grid * l / n;  // CTAs of layer l
     for (uint32_t b = 0; b < g_l; ++b, ++cta) {
@@ -866,6 +913,7 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
       p.cta_e0[cta] = host_row_ptrs[l][std::min(r0, G.rows)];
       p.cta_e1[cta] = host_row_ptrs[l][std::min(r1, G.rows)];
       p.nq_max = std::max(p.nq_max, q1 - q0);
+      ent_max = std::max(ent_max, p.cta_e1[cta] - p.cta_e0[cta]);
       if (r1 > r0) so_rows_max = std::max(so_rows_max, (r1 - 1) / G.group2 - r0 / G.group2 + 1);
     }
   }
@@ -875,8 +923,11 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   const size_t x_bytes = p.xsm ? align_up((size_t)G.cols * 4 + 4, 16) : 0;  // + the pads' zero slot
   const uint32_t tmax = (p.kmax <= 2 && p.uniform_rb && p.xsm && p.uq == 2) ? 2u : 1u;
   const size_t win_bytes = (size_t)p.warps * tmax * kWinWords * 4;
+  // the CTA's outlier entries staged by one bulk copy when they fit
+  const size_t ent_bytes = align_up(((size_t)ent_max + 3) * 4, 16);
+  p.csr_stage = ent_max > 0 && ent_bytes <= (size_t)env_u32("QW_CSR_STAGE_KB", 32) * 1024;
   const size_t fixed = align_up(so_bytes, 16) + part_bytes + align_up(misc_bytes, 16) + x_bytes +
-                       win_bytes + 64;
+                       win_bytes + 64 + (p.csr_stage ? ent_bytes + 16 : 0) + 8;
   // precomputed 1st-order scales: one uint2 per (slot, quad, k, lane)
   auto pre_bytes = [&](size_t s) { return p.teams == 2 ? (size_t)0 : s * p.uq * p.kmax * p.warps * 32 * 8; };
   // ring: the CTA's whole quad range when it fits in ~half an SM (so the next
@@ -907,8 +958,9 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   p.xg_off = p.misc_off + (uint32_t)align_up(misc_bytes, 16);
   p.win_off = p.xg_off + (uint32_t)x_bytes;
   p.pre_off = p.win_off + (uint32_t)win_bytes;
-  p.bar_off = (uint32_t)align_up(p.pre_off + pre_bytes(S), 8);
-  p.smem = (uint32_t)(p.bar_off + (2 * S + 2) * 8);
+  p.ent_off = (uint32_t)align_up(p.pre_off + pre_bytes(S), 16);
+  p.bar_off = (uint32_t)align_up(p.ent_off + (p.csr_stage ? ent_bytes : 0), 8);
+  p.smem = (uint32_t)(p.bar_off + (2 * S + 3) * 8);
   // launch policy (fixed at plan time; the env knobs are diagnostics).  A CTA
   // that owns its SM (teams / wide) starts after its predecessor: no scale
   // precompute (the main loop must run under the weight stream), x first, and
@@ -985,6 +1037,7 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   a.grid = p.grid, a.nq_max = p.nq_max, a.rb_magic = p.rb_magic, a.rb_one = p.rb_one;
   a.so_off = p.so_off, a.part_off = p.part_off, a.csr_off = p.misc_off, a.x_off = p.xg_off, a.win_off = p.win_off, a.pre_off = p.pre_off;
   a.bar_off = p.bar_off;
+  a.ent_off = p.ent_off, a.csr_stage = p.csr_stage;
   a.pf_n = p.pf_n;
   a.pf_late = p.pf_late;
   for (uint32_t r = 0; r < GemvPlan::kMaxPf; ++r) a.pf_ptr[r] = p.pf_ptr[r], a.pf_bytes[r] = p.pf_bytes[r];
@@ -1038,7 +1091,7 @@ int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
 // rows, FHFMA, window reduction), so the results equal the K2 launches'.
 namespace {
 constexpr uint32_t kChainCons = 16, kChainThreads = (kChainCons + 2) * 32;
-constexpr uint32_t kChainEmpty = 720720;  // lcm(1..16): divisible by every team size W
+constexpr uint32_t kChainEmpty = kChainCons;  // every consumer warp hands every unit back
 // team 0 hands its prepared X to team 1 (saves the duplicate prologue); off:
 // with both KG bodies in one kernel ptxas spills heavily at the 96-register cap
 constexpr bool kChainShareX = false;
@@ -1079,9 +1132,7 @@ struct ChainCtx {
   float s_scale;
   uint32_t gu, nunit, nrows, q0, rb_first, team, wt, S, slot_bytes;
 };
-__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
+
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const unsigned* p) {
   uint32_t v;
@@ -1092,16 +1143,47 @@ __device__ __forceinline__ void red_release_gpu(unsigned* p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Chain diagnostics: with a watch buffer, a wait that spins for ~seconds
+// records (code, step, unit/parity, CTA, warp) and traps instead of hanging.
+__device__ unsigned* g_chain_watch = nullptr;
+__device__ __forceinline__ void chain_wait(uint64_t* bar, uint32_t parity, uint32_t code, uint32_t arg) {
+  if (!g_chain_watch) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  for (uint32_t i = 0; !mbar_try_wait(bar, parity); ++i) {
+    if (i == (1u << 22)) {
+      unsigned* w = g_chain_watch + 8 * (blockIdx.x * 32 + (threadIdx.x >> 5));
+      w[0] = 1u + code, w[1] = arg, w[2] = parity, w[3] = blockIdx.x, w[4] = threadIdx.x;
+      __threadfence_system();
+      __trap();
+    }
+  }
+}
+
 template <int KG, int NQ>
 __device__ __forceinline__ void chain_consume(const ChainStep& st, const ChainCtx& c) {
   const Geometry G = st.g;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t W = st.W, W2 = st.W2, W4 = W - W2, T = st.T, team = c.team, wt = c.wt;
   const uint32_t dense = G.dense_bytes, nunit = c.nunit;
-  if (team >= T) return;  // idle warp this step (W does not divide 16)
-  // ring position of the step's first unit
+  // ring position of the step's first unit.  EVERY consumer warp waits for
+  // and hands back EVERY unit (the owning team after decoding it): a slot is
+  // refilled only when all 16 warps are done with it, so no warp can fall two
+  // phases behind a slot and misread a parity.
   uint32_t slot = c.gu % c.S, phase = (c.gu / c.S) & 1u;
-  const uint32_t arrive_count = kChainEmpty / W;
+  auto pass = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&c.empty[slot]);
+    if (++slot == c.S) slot = 0, phase ^= 1u;
+  };
+  if (team >= T) {  // idle warp this step (W does not divide 16)
+    for (uint32_t u = 0; u < nunit; ++u) {
+      chain_wait(&c.full[slot], phase, 1, c.gu + u);
+      pass();
+    }
+    return;
+  }
   const uint32_t rb_magic = st.rb_magic, rb_one = st.rb_one;
   auto row_block = [&](uint32_t r) { return rb_one ? r : __umulhi(r, rb_magic); };
   const bool two = wt < W2;
@@ -1262,9 +1344,13 @@ __device__ __forceinline__ void chain_consume(const ChainStep& st, const ChainCt
       // every unit's phase is observed in order (a parity wait that skipped a
       // phase could alias with an older completed one); only the team's own
       // units (u = team mod T) are decoded
-      mbar_wait(&c.full[slot], phase);
+      if (g_chain_watch && lane == 0) {  // diagnostics: progress (unit being waited for)
+        volatile unsigned* w = g_chain_watch + 8 * (blockIdx.x * 32 + (threadIdx.x >> 5));
+        w[5] = c.gu + u + 1, w[6] = slot, w[7] = phase;
+      }
+      chain_wait(&c.full[slot], phase, 1, c.gu + u);
       if (owner != team) {
-        if (++slot == c.S) slot = 0, phase ^= 1u;
+        pass();
         continue;
       }
       const uint8_t* sb = c.ring + (size_t)slot * c.slot_bytes;
@@ -1316,9 +1402,7 @@ __device__ __forceinline__ void chain_consume(const ChainStep& st, const ChainCt
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cnt(&c.empty[slot], arrive_count);
-      if (++slot == c.S) slot = 0, phase ^= 1u;
+      pass();
 #pragma unroll
       for (int j = 0; j < NQ; ++j)
         *reinterpret_cast<float4*>(win + win_base(lane) + wrow + 4 * j) =
@@ -1369,7 +1453,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
 
   if (threadIdx.x < a.S) {
     mbar_init(&full[threadIdx.x], 1);
-    mbar_init(&empty[threadIdx.x], kChainEmpty);  // the owning team's W warps arrive with kChainEmpty / W
+    mbar_init(&empty[threadIdx.x], kChainEmpty);
   }
   if (threadIdx.x == 32) {
     mbar_init(&so_full[0], 1), mbar_init(&so_full[1], 1);
@@ -1392,7 +1476,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
         const uint32_t nq = cc.q1 - cc.q0, NQ = st.NQ, dense = G.dense_bytes;
         const uint32_t r_begin = cc.q0 * kRowsPerQuad, r_end = min(cc.q1 * kRowsPerQuad, G.rows);
         const uint32_t sb = s & 1u;
-        if (s >= 2) mbar_wait(&so_empty[sb], ((s >> 1) - 1u) & 1u);  // step s-2 done with the buffer
+        if (s >= 2) chain_wait(&so_empty[sb], ((s >> 1) - 1u) & 1u, 2, s);  // step s-2 done with the buffer
         const uint32_t so_bytes =
             r_end > r_begin ? (row_block(r_end - 1) - row_block(r_begin) + 1) * G.G2s * 4u : 0u;
         if (so_bytes) {
@@ -1406,7 +1490,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
         const uint32_t nunit = (nq + NQ - 1) / NQ;
         for (uint32_t u = 0; u < nunit; ++u, ++gu) {
           const uint32_t bytes = min(NQ, nq - NQ * u) * dense;
-          if (gu >= a.S) mbar_wait(&empty[slot], phase ^ 1u);
+          if (g_chain_watch) {
+            volatile unsigned* w = g_chain_watch + 8 * (blockIdx.x * 32 + 16);
+            w[5] = gu + 1, w[6] = slot, w[7] = phase;
+          }
+          if (gu >= a.S) chain_wait(&empty[slot], phase ^ 1u, 3, gu);
           mbar_expect_tx(&full[slot], bytes);
           bulk_load_nohint(smem + (size_t)slot * a.slot_bytes, src, bytes, &full[slot]);
           src += bytes;
@@ -1443,7 +1531,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
       };
       if (n) fetch(0);
       __syncwarp();
-      mbar_wait(xbar, s & 1u);  // x of step s staged
+      chain_wait(xbar, s & 1u, 4, s);  // x of step s staged
       uint32_t t0 = 0;
       for (uint32_t c0 = 0; c0 < n; c0 += 32u * kPer) {
         const uint32_t c1 = min(c0 + 32u * kPer, n);
@@ -1503,7 +1591,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
       named_sync(1, kChainCons * 32);
       if (threadIdx.x == 0) mbar_arrive(xbar);
     }
-    mbar_wait(&so_full[s & 1u], (s >> 1) & 1u);
+    chain_wait(&so_full[s & 1u], (s >> 1) & 1u, 5, s);
     ChainCtx c;
     c.ring = ring;
     c.s_so = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(s_so) + (s & 1u) * a.so_stride);
@@ -1540,6 +1628,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
   }
 }
 }  // namespace
+
+unsigned*& chain_watch_host() {
+  static unsigned* p = nullptr;
+  return p;
+}
+const unsigned* chain_watch() { return chain_watch_host(); }
 
 struct ChainPlan {
   ChainArgs args{};
@@ -1632,6 +1726,17 @@ int plan_chain(ChainPlan** out, const ChainStepDesc* steps, uint32_t n, int num_
     e = cudaMemcpy((uint8_t*)p->dmem + bytes_steps, hc.data(), sizeof(ChainCta) * hc.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
+  if (e == cudaSuccess && std::getenv("QW_CHAIN_WATCH")) {  // diagnostics: hang -> record + trap
+    static unsigned* host_watch = nullptr;
+    if (!host_watch) {
+      e = cudaHostAlloc((void**)&host_watch, 148 * 32 * 8 * 4 * 4, cudaHostAllocMapped);
+      if (e == cudaSuccess) std::memset(host_watch, 0, 148 * 32 * 8 * 4 * 4);
+    }
+    unsigned* dptr = nullptr;
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&dptr, host_watch, 0);
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_chain_watch, &dptr, sizeof(dptr));
+    chain_watch_host() = host_watch;
+  }
   if (e != cudaSuccess) {
     free_chain(p);
     return (int)e;

@@ -1,11 +1,7 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; grep -E "passed|failed" gpurun_out/pytest_gpu.log | tail -1
+echo "== L=1 watch"; QW_CHAIN_WATCH=1 timeout 120 python scripts/_dbg_hang2.py 1 2>&1 | tail -2
+echo "== L=1"; timeout 120 python scripts/_dbg_hang2.py 1 2>&1 | tail -1
+echo "== L=2"; timeout 120 python scripts/_dbg_hang2.py 2 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 120 > gpurun_out/pytest_gpu.log 2>&1; grep -E "passed|failed" gpurun_out/pytest_gpu.log | tail -1
 timeout 600 python bench.py --no-cpu --steps 10 > gpurun_out/b.json 2> gpurun_out/b.err
 python -c "import json;d=json.load(open('gpurun_out/b.json'));print(d['value'],d['independent']['value'],d['chain_kernel']['value'],d['roofline']['achieved'])"
-timeout 1200 python scripts/shape_sweep.py > gpurun_out/shape_sweep.jsonl 2> gpurun_out/shape_sweep.err
-python - <<'P'
-import json
-for l in open("gpurun_out/shape_sweep.jsonl"):
-    d = json.loads(l); print(d["case"], d["us_per_call"], d["gb_s"], d["pct_of_hbm_peak"], "%.1e" % d["rel_l2_vs_f64"])
-P
-timeout 600 python scripts/batch_sweep.py > gpurun_out/batch_sweep.jsonl 2> gpurun_out/batch_sweep.err; tail -2 gpurun_out/batch_sweep.err
