@@ -206,7 +206,7 @@ int qw_group_set_prefetch(qw_group* group, const qw_layer* const* next, uint32_t
  * whole sequence (a counter reset + 1 kernel, CUDA-graph capturable).
  * Results equal the per-step launches' (qw_group_matvec / qw_matvec_ex).
  * QW_ERR_UNSUPPORTED: a step geometry the chain kernel does not cover
- * (group2 % 4 != 0, more than 12288 columns). */
+ * (group2 % 4 != 0, more than 16384 columns). */
 typedef struct qw_chain qw_chain;
 typedef struct {
   const qw_layer* const* layers; /* n layers, identical geometry */

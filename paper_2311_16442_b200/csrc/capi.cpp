@@ -825,7 +825,7 @@ int qw_chain_create(const qw_chain_step* steps, uint32_t n, qw_chain** out) {
     const int e = qwdev::plan_chain(&C->plan, d.data(), n, num_sms);
     if (e == (int)cudaErrorInvalidValue) return fail(QW_ERR_ARG, "chain: a step's layers differ in geometry");
     if (e == (int)cudaErrorNotSupported)
-      return fail(QW_ERR_UNSUPPORTED, "chain: step geometry not covered (group2 % 4 != 0 or > 12288 columns)");
+      return fail(QW_ERR_UNSUPPORTED, "chain: step geometry not covered (group2 % 4 != 0 or > 16384 columns)");
     if (e) return cuda_fail((cudaError_t)e, "chain plan");
     *out = C.release();
     return (int)QW_OK;

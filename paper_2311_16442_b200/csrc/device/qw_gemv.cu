@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <cstdint>
@@ -879,7 +880,7 @@ int plan_geometry(GemvPlan& p, const Geometry& G) {
   while (p.kmax < 4 && warps_for(p.kmax) > (p.kmax <= 2 ? 8u : 15u)) ++p.kmax;
   if (warps_for(p.kmax) > 15) return (int)cudaErrorInvalidConfiguration;
   p.uniform_rb = (G.group2 % kRowsPerQuad) == 0;
-  p.xsm = G.cols <= 12288;
+  p.xsm = G.cols <= 16384;  // x staged in shared memory (64 KB at most)
   // wide layers (down_proj): KG = 2 over up to 16 warps in one CTA per SM
   // rather than KG >= 3 (register spills) in two
   p.wide = p.kmax > 2 && warps_for(2) <= 16 && p.uniform_rb && p.xsm && env_u32("QW_WIDE", 1);
@@ -921,29 +922,48 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   const size_t part_bytes = (size_t)p.nq_max * p.warps * 16;  // [row][warp of a team]
   const size_t misc_bytes = (size_t)p.nq_max * 4 * 4 + ((size_t)p.nq_max * 4 + 4) * 4 + 256 * 4 + 64 * 4;
   const size_t x_bytes = p.xsm ? align_up((size_t)G.cols * 4 + 4, 16) : 0;  // + the pads' zero slot
-  const uint32_t tmax = (p.kmax <= 2 && p.uniform_rb && p.xsm && p.uq == 2) ? 2u : 1u;
+  const uint32_t tmax = (!p.wide && p.kmax <= 2 && p.uniform_rb && p.xsm && p.uq == 2) ? 2u : 1u;
   const size_t win_bytes = (size_t)p.warps * tmax * kWinWords * 4;
-  // the CTA's outlier entries staged by one bulk copy when they fit
+  // long ranges (group launches, big layers): two teams, the whole SM
+  p.teams = (!p.wide && p.nq_max >= env_u32("QW_TEAMS_MIN_NQ", 4) && p.kmax <= 2 && p.uniform_rb && p.xsm &&
+             p.uq == 2) ? 2 : 1;
+  // the CTA's outlier entries staged by one bulk copy when they fit and do
+  // not cost a ring slot (decided below)
   const size_t ent_bytes = align_up(((size_t)ent_max + 3) * 4, 16);
-  p.csr_stage = ent_max > 0 && ent_bytes <= (size_t)env_u32("QW_CSR_STAGE_KB", 32) * 1024;
+  size_t stage_bytes = 0;
   const size_t fixed = align_up(so_bytes, 16) + part_bytes + align_up(misc_bytes, 16) + x_bytes +
-                       win_bytes + 64 + (p.csr_stage ? ent_bytes + 16 : 0) + 8;
+                       win_bytes + 64 + 8;
   // precomputed 1st-order scales: one uint2 per (slot, quad, k, lane)
   auto pre_bytes = [&](size_t s) { return p.teams == 2 ? (size_t)0 : s * p.uq * p.kmax * p.warps * 32 * 8; };
   // ring: the CTA's whole quad range when it fits in ~half an SM (so the next
   // layer's CTA fits beside it under PDL), else as many slots as fit
   const size_t unit_bytes = (size_t)p.uq * G.dense_bytes;
   const size_t units = (p.nq_max + p.uq - 1) / p.uq;
-  // long ranges (group launches, big layers): two teams, the whole SM
-  p.teams = (!p.wide && p.nq_max >= env_u32("QW_TEAMS_MIN_NQ", 4) && p.kmax <= 2 && p.uniform_rb && p.xsm &&
-             p.uq == 2) ? 2 : 1;
   const size_t half_sm = (p.teams == 2 || p.wide ? 200 : env_u32("QW_SMEM_KB", 112)) * 1024, full_sm = 220 * 1024;
-  size_t S = units;
   auto total_b = [&](size_t s) {
-    return align_up(s * unit_bytes, 128) + fixed + pre_bytes(s) + (2 * s + 2) * 8;
+    return align_up(s * unit_bytes, 128) + fixed + stage_bytes + pre_bytes(s) + (2 * s + 2) * 8;
   };
-  while (S > 3 && total_b(S) > half_sm) --S;
-  while (S > 2 && total_b(S) > full_sm) --S;
+  auto slots = [&]() {
+    size_t s = units;
+    while (s > 3 && total_b(s) > half_sm) --s;
+    while (s > 2 && total_b(s) > full_sm) --s;
+    return s;
+  };
+  size_t S = slots();
+  // (x staged in shared memory only: the per-row sums gather x; a CTA that
+  // owns its SM trades ring slots for it, a co-resident one must keep its fit)
+  p.csr_stage = 0;
+  if (p.xsm && ent_max > 0 && ent_bytes <= (size_t)env_u32("QW_CSR_STAGE_KB", 32) * 1024) {
+    stage_bytes = ent_bytes + 16;
+    const size_t S1 = slots();
+    const bool alone = p.teams == 2 || p.wide;
+    const bool ok = alone ? (S1 >= 2 && total_b(S1) <= full_sm)
+                          : (S1 == S && (total_b(S1) <= half_sm || total_b(S) > half_sm));
+    if (ok)
+      p.csr_stage = 1, S = S1;
+    else
+      stage_bytes = 0;
+  }
   // two teams share a ring: with an even slot count slot s only ever holds
   // team (s % 2)'s units, so a team's successive units in a slot are
   // successive barrier phases.  (With an odd count a fast team could wait for
@@ -967,6 +987,12 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   // the producer holds the stream after 4 units until x is staged.  Otherwise
   // (two CTAs per SM under PDL) the resident units' scales are precomputed
   // while the predecessor still runs.
+  if (env_u32("QW_PLAN_DEBUG", 0))
+    std::fprintf(stderr,
+                 "qw plan: rows %u cols %u kmax %u warps %u teams %u wide %d xsm %u nq_max %u slots %u unit %zu B "
+                 "smem %u csr_stage %u (entries %u)\n",
+                 G.rows, G.cols, p.kmax, p.warps, p.teams, (int)p.wide, p.xsm, p.nq_max, p.nslot, unit_bytes, p.smem,
+                 p.csr_stage, ent_max);
   const bool alone = p.teams == 2 || p.wide;
   p.pre = env_u32("QW_NO_PRE", 0) ? 0u : 1u;
   p.npre_max = env_u32("QW_NPRE_MAX", alone ? 0u : 1000000u);

@@ -11,4 +11,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -c 4 -o gpurun_out/prof_gemv python scripts/step_timeline.py 1 > gpurun_out/ncu_full.out 2>&1; tail -1 gpurun_out/ncu_full.out
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:chain_kernel -s 1 -c 1 -o gpurun_out/prof_chain python scripts/prof_chain.py 1 1 > gpurun_out/ncu_chain.out 2>&1; tail -1 gpurun_out/ncu_chain.out
 timeout 600 python scripts/batch_sweep.py > gpurun_out/batch_sweep.jsonl 2> gpurun_out/batch_sweep.err; tail -3 gpurun_out/batch_sweep.jsonl
+timeout 1200 python scripts/shape_sweep.py > gpurun_out/shape_sweep.jsonl 2> gpurun_out/shape_sweep.err; tail -3 gpurun_out/shape_sweep.jsonl
 ls -la gpurun_out | head -40
