@@ -997,7 +997,7 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   p.pre = env_u32("QW_NO_PRE", 0) ? 0u : 1u;
   p.npre_max = env_u32("QW_NPRE_MAX", alone ? 0u : 1000000u);
   p.x_first = env_u32("QW_XFIRST", alone ? 1u : 0u);
-  p.x_gate = env_u32("QW_XGATE", alone ? 4u : 1000000u);
+  p.x_gate = env_u32("QW_XGATE", alone ? 1u : 1000000u);
   p.pf_late = env_u32("QW_PF_LATE", 1);
   static bool attr_set = false;  // raise the opt-in limit once per process
   if (!attr_set) {
