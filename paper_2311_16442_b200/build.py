@@ -40,7 +40,7 @@ def _cuda_home() -> Path:
 def _sources():
     host = sorted((CSRC / "host").glob("*.cpp")) + [CSRC / "capi.cpp"]
     dev = sorted((CSRC / "device").glob("*.cu"))
-    headers = (sorted(CSRC.rglob("*.hpp")) + sorted(CSRC.rglob("*.inl")) +
+    headers = (sorted(CSRC.rglob("*.hpp")) + sorted(CSRC.rglob("*.cuh")) + sorted(CSRC.rglob("*.inl")) +
                [ROOT / "include" / "qweight_b200.h"])
     return host, dev, headers
 

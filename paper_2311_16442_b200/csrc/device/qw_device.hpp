@@ -108,6 +108,9 @@ struct Workspace {
   uint32_t* flags = nullptr;
 };
 
+// Geometry-dependent part of a batch-1 plan (warps, groups per lane, quads
+// per slot, wide/x-staging decisions); cudaErrorInvalidConfiguration if too wide.
+int plan_geometry(GemvPlan& p, const Geometry& G);
 // Launchers (return cudaError_t as int).
 // Fill L.plan for a device with num_sms SMs (returns cudaError_t).
 int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr);
