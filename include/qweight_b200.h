@@ -180,9 +180,10 @@ int qw_matvec_pdl(const qw_layer* layer, const float* x, uint32_t batch,
                                       reading it (q/k/v, gate/up share inputs) */
 int qw_matvec_ex(const qw_layer* layer, const float* x, uint32_t batch, float* y,
                  qw_workspace* ws, void* stream, uint32_t flags);
-/* Group launch (batch 1): up to 4 layers with identical geometry that read
- * the same activation (q/k/v, gate/up) in ONE fused launch -- one dependency
- * wait, one activation staging.  The layers must outlive the group.
+/* Group launch (batch 1): up to 4 layers that read the same activation
+ * (q/k/v, gate/up) in ONE fused launch -- one dependency wait, one activation
+ * staging.  The layers share cols, channel split and group2; rows may differ
+ * (GQA q/k/v).  The layers must outlive the group.
  * ys[i]: device fp32 [rows] output of layers[i]. */
 typedef struct qw_group qw_group;
 int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out);

@@ -739,7 +739,7 @@ int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out) {
     cudaSetDevice(G->device);
     const int e = qwdev::plan_gemv_group(G->plan, G->layers.data(), rps.data(), n, layers[0]->num_sms);
     if (e == (int)cudaErrorInvalidValue)
-      return fail(QW_ERR_ARG, "group: layers must share rows, cols, channel split and group2");
+      return fail(QW_ERR_ARG, "group: layers must share cols, channel split and group2 (rows may differ)");
     if (e) return cuda_fail((cudaError_t)e, "group plan");
     *out = G.release();
     return (int)QW_OK;

@@ -63,6 +63,7 @@ struct GemvArgs {
   const uint16_t* perm[kMaxSeg];
   float* y[kMaxSeg];
   float s_scale[kMaxSeg];  // 2^-P: keeps (eff - zero2) scale2 2^-P inside fp16
+  uint32_t seg_rows[kMaxSeg];  // output rows of each layer (a group may mix row counts: GQA q/k/v)
   const float* x;
   Geometry g;
   uint32_t W, W2, T, S, grid, nq_max;  // warps per team, 2-bit warps, teams, ring slots
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
   const uint32_t nunit = (nq + NQ - 1) / NQ;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t r_begin = q0 * kRowsPerQuad;
-  const uint32_t r_end = min(q1 * kRowsPerQuad, G.rows);
+  const uint32_t seg_rows = a.seg_rows[seg];
+  const uint32_t r_end = min(q1 * kRowsPerQuad, seg_rows);
   const uint32_t nrows = r_end - r_begin;
   auto row_block = [&](uint32_t r) { return a.rb_one ? r : __umulhi(r, a.rb_magic); };
   const uint32_t rb_first = row_block(r_begin);
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
         float A[4], Cz[4];
 #pragma unroll
         for (int i = 0; i < (UNI ? 1 : 4); ++i) {
-          const uint32_t rb = row_block(min(r0 + i, G.rows - 1)) - rb_first;
+          const uint32_t rb = row_block(min(r0 + i, seg_rows - 1)) - rb_first;
           const uint32_t e = s_so[rb * G.G2s + gk[k]];
           A[i] = half_bits_to_float(e) * s_scale;  // exact: scale2 * 2^-P
           Cz[i] = -(pow2f(10 - pe[k]) + small_int_to_float(e >> 16));
@@ -770,24 +772,42 @@ int plan_geometry(GemvPlan& p, const Geometry& G) {
 namespace {
 
 // CTA ranges (one layer each) + shared-memory layout for the largest range
-int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_ptrs, uint32_t n, int num_sms) {
+int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_ptrs, const uint32_t* seg_rows,
+              uint32_t n, int num_sms) {
   uint32_t per_sm = 1;
   if (const char* e = std::getenv("QW_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
-  const uint64_t total = (uint64_t)n * G.quads;
+  uint64_t total = 0;
+  uint32_t lq[kMaxSeg];
+  for (uint32_t l = 0; l < n; ++l) lq[l] = (seg_rows[l] + kRowsPerQuad - 1) / kRowsPerQuad, total += lq[l];
   uint32_t grid = (uint32_t)std::min<uint64_t>(std::min<uint32_t>((uint32_t)num_sms * per_sm, kMaxGrid), total);
   grid = std::max(grid, n);
   p.grid = grid;
   p.nq_max = 0;
+  // CTAs per layer in proportion to its quads (equal layers: an equal split)
+  uint32_t gl[kMaxSeg], given = 0;
+  uint64_t acc = 0;
+  for (uint32_t l = 0; l < n; ++l) {
+    acc += lq[l];
+    const uint32_t upto = (uint32_t)(grid * acc / total);
+    gl[l] = std::max<uint32_t>(1, std::min<uint32_t>(lq[l], upto > given ? upto - given : 1));
+    given += gl[l];
+  }
+  while (given > grid) {  // rounding with the >= 1 floor: take CTAs back from the largest share
+    uint32_t m = 0;
+    for (uint32_t l = 1; l < n; ++l) m = gl[l] > gl[m] ? l : m;
+    --gl[m], --given;
+  }
+  p.grid = grid = given;
   uint32_t so_rows_max = 0, cta = 0, ent_max = 0;
   for (uint32_t l = 0; l < n; ++l) {
-    const uint32_t g_l = grid * (l + 1) / n - grid * l / n;  // CTAs of layer l
+    const uint32_t g_l = gl[l], quads = lq[l], rows = seg_rows[l];  // CTAs / quads / rows of layer l
     for (uint32_t b = 0; b < g_l; ++b, ++cta) {
-      const uint32_t q0 = (uint32_t)((uint64_t)b * G.quads / g_l), q1 = (uint32_t)((uint64_t)(b + 1) * G.quads / g_l);
+      const uint32_t q0 = (uint32_t)((uint64_t)b * quads / g_l), q1 = (uint32_t)((uint64_t)(b + 1) * quads / g_l);
       p.cta_seg[cta] = (uint8_t)l;
       p.cta_q0[cta] = q0, p.cta_q1[cta] = q1;
-      const uint32_t r0 = q0 * kRowsPerQuad, r1 = std::min(q1 * kRowsPerQuad, G.rows);
-      p.cta_e0[cta] = host_row_ptrs[l][std::min(r0, G.rows)];
-      p.cta_e1[cta] = host_row_ptrs[l][std::min(r1, G.rows)];
+      const uint32_t r0 = q0 * kRowsPerQuad, r1 = std::min(q1 * kRowsPerQuad, rows);
+      p.cta_e0[cta] = host_row_ptrs[l][std::min(r0, rows)];
+      p.cta_e1[cta] = host_row_ptrs[l][std::min(r1, rows)];
       p.nq_max = std::max(p.nq_max, q1 - q0);
       ent_max = std::max(ent_max, p.cta_e1[cta] - p.cta_e0[cta]);
       if (r1 > r0) so_rows_max = std::max(so_rows_max, (r1 - 1) / G.group2 - r0 / G.group2 + 1);
@@ -904,7 +924,8 @@ int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
   GemvPlan& p = L.plan;
   if (int e = plan_geometry(p, L.g)) return e;
   const uint32_t* rp[1] = {host_row_ptr};
-  return plan_ctas(p, L.g, rp, 1, num_sms);
+  const uint32_t rows[1] = {L.g.rows};
+  return plan_ctas(p, L.g, rp, rows, 1, num_sms);
 }
 
 int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_t* const* host_row_ptrs,
@@ -913,12 +934,16 @@ int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_
   const Geometry& G = layers[0]->g;
   for (uint32_t l = 1; l < n; ++l) {
     const Geometry& H = layers[l]->g;
-    if (H.rows != G.rows || H.cols != G.cols || H.n4 != G.n4 || H.n2p != G.n2p || H.group2 != G.group2 ||
-        H.dense_bytes != G.dense_bytes)
+    // one decode body for all: same columns, channel split and 2-order group;
+    // the row counts may differ (GQA q/k/v)
+    if (H.cols != G.cols || H.n4 != G.n4 || H.n2p != G.n2p || H.group2 != G.group2 || H.dense_bytes != G.dense_bytes ||
+        H.G2s != G.G2s)
       return (int)cudaErrorInvalidValue;
   }
   p = layers[0]->plan;  // geometry part is identical
-  return plan_ctas(p, G, host_row_ptrs, n, num_sms);
+  uint32_t rows[kMaxSeg];
+  for (uint32_t l = 0; l < n; ++l) rows[l] = layers[l]->g.rows;
+  return plan_ctas(p, G, host_row_ptrs, rows, n, num_sms);
 }
 
 int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
@@ -931,6 +956,7 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
     a.quads[l] = L.quads, a.sorder[l] = L.sorder, a.row_ptr[l] = L.row_ptr;
     a.csr[l] = L.csr, a.perm[l] = L.perm16, a.s_scale[l] = L.plan.s_scale;
     a.y[l] = ys[std::min(l, n - 1)];
+    a.seg_rows[l] = L.g.rows;
   }
   a.x = x;
   a.g = G;

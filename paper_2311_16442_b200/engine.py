@@ -246,9 +246,10 @@ def upload(layer: PackedLayer, device: int = 0) -> DeviceLayer:
 
 
 class LayerGroup:
-    """Several DeviceLayers of identical geometry that read the same input
-    (q/k/v, gate/up) computed by ONE fused batch-1 launch (qw_group_matvec):
-    the dependency wait and the activation staging are paid once."""
+    """Several DeviceLayers that read the same input (q/k/v, gate/up) computed
+    by ONE fused batch-1 launch (qw_group_matvec): the dependency wait and the
+    activation staging are paid once.  The layers share their columns,
+    channel split and group2; the row counts may differ (GQA: q with k/v)."""
 
     def __init__(self, layers: list["DeviceLayer"]):
         self.layers = list(layers)

@@ -59,3 +59,40 @@ for name, rows, cols, g2, ratio in cases:
                       "us_per_call": round(us, 3), "gb_s": round(balg / us / 1e3, 1),
                       "pct_of_hbm_peak": round(100 * balg / us / 1e3 / PEAK, 1), "rel_l2_vs_f64": rel,
                       "copies": n}), flush=True)
+
+# GQA q/k/v of Llama-2-70B as ONE group launch (rows 8192 + 1024 + 1024)
+layers = [qw.synth_layer(r, 8192, seed=30 + i) for i, r in enumerate((8192, 1024, 1024))]
+n = 8
+groups, outs = [], []
+for c in range(n):
+    dls = [qw.DeviceLayer(L) for L in layers]
+    groups.append(qw.LayerGroup(dls))
+    outs.append([torch.empty(L.cfg.rows, device="cuda") for L in layers])
+x = torch.from_numpy(qw.synth_activation(8192, 8)).cuda()
+
+
+def run_g():
+    for g_, o in zip(groups, outs):
+        g_.matvec(x, outs=o, pdl=True)
+run_g()
+torch.cuda.synchronize()
+rel = max(float(np.linalg.norm(o.cpu().numpy() - oracle.matvec_f64(L, x.cpu().numpy())) /
+                np.linalg.norm(oracle.matvec_f64(L, x.cpu().numpy()))) for L, o in zip(layers, outs[0]))
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    run_g()
+for _ in range(3):
+    g.replay()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10):
+    g.replay()
+e1.record()
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1e3 / (10 * n)
+balg = sum(qw.payload_bytes(L) + 4 * (L.cfg.rows + L.cfg.cols) for L in layers)
+print(json.dumps({"case": "cfg5 70B q/k/v GQA group launch", "rows": 10240, "cols": 8192, "group2": 16,
+                  "outlier_ratio": 0.002, "nnz": int(sum(L.nnz for L in layers)), "us_per_call": round(us, 3),
+                  "gb_s": round(balg / us / 1e3, 1), "pct_of_hbm_peak": round(100 * balg / us / 1e3 / PEAK, 1),
+                  "rel_l2_vs_f64": rel, "copies": n}), flush=True)

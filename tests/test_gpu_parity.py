@@ -353,3 +353,19 @@ def test_team_ring_is_race_free():
     for _ in range(20):
         for d in dls:
             assert torch.equal(d.matvec(x, pdl=True), first)
+
+
+def test_group_launch_with_unequal_rows_gqa():
+    """GQA-style group: q (512 rows) with k and v (128 rows each) in one launch,
+    CTAs split in proportion to the quads; bitwise equal to single launches."""
+    torch = _torch()
+    layers = [qw.synth_layer(r, 1024, seed=120 + i, outlier_ratio=0.005) for i, r in enumerate((512, 128, 128))]
+    dls = [qw.DeviceLayer(L) for L in layers]
+    grp = qw.LayerGroup(dls)
+    x = qw.synth_activation(1024, 121)
+    xd = torch.from_numpy(x).cuda()
+    outs = grp.matvec(xd)
+    for L, d, o in zip(layers, dls, outs):
+        assert o.shape[0] == L.cfg.rows
+        assert rel_l2(o.cpu().numpy(), oracle.matvec_f64(L, x)) <= TOL
+        assert torch.equal(o, d.matvec(xd))
