@@ -235,9 +235,12 @@ def test_tp_linear_single_rank_nccl(mode):
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
     layer = qw.synth_layer(256, 1024, seed=9, outlier_ratio=0.005)
     x = qw.synth_activation(1024, 10)
-    tp = TPLinear(layer, 0, 1, mode, device="cuda:0")
-    y = tp.forward(torch.from_numpy(x).cuda()).cpu().numpy()
-    assert rel_l2(y, oracle.matvec_f64(layer, x)) <= TOL
+    try:
+        tp = TPLinear(layer, 0, 1, mode, device="cuda:0")
+        y = tp.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert rel_l2(y, oracle.matvec_f64(layer, x)) <= TOL
+    finally:
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------- group launch
