@@ -416,7 +416,10 @@ def run_ours(args):
             "e2e": {"value": round(world * step_bytes / (e2e_ms * 1e6), 2), "unit": "GB/s",
                     "h2d_bytes_per_step": stack.h2d_bytes, "d2h_bytes_per_step": stack.d2h_bytes,
                     "ms_per_step": round(e2e_ms, 4),
-                    "api": "LinearStack.run (pinned H2D, graph, D2H, sync)"},
+                    "api": "LinearStack.run: one CUDA graph -- pinned H2D in growing chunks on a copy stream "
+                           "ahead of the launches that read them, the launches, D2H in shrinking chunks on a "
+                           "second copy stream as launches finish -- then sync"
+                           if not chain else "LinearStack.run (pinned H2D, chain kernel, D2H, sync)"},
             "gpu_launches": (1 if chain else len(stack.groups)) * args.steps,
             "clocks": clocks,
             "prep_s": round(prep_s, 1),

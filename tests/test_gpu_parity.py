@@ -372,3 +372,23 @@ def test_group_launch_with_unequal_rows_gqa():
         assert o.shape[0] == L.cfg.rows
         assert rel_l2(o.cpu().numpy(), oracle.matvec_f64(L, x)) <= TOL
         assert torch.equal(o, d.matvec(xd))
+
+
+def test_linear_stack_run_end_to_end():
+    """LinearStack.run (the e2e API): host inputs -> one graph with the copies
+    overlapped -> host outputs; equals the per-layer launches, twice in a row."""
+    from paper_2311_16442_b200.stack import LinearStack
+    torch = _torch()
+    shapes = [(512, 1024), (512, 1024), (256, 512), (1024, 256)]
+    layers = [qw.synth_layer(r, c, seed=140 + i) for i, (r, c) in enumerate(shapes)]
+    dls = [qw.DeviceLayer(L) for L in layers]
+    st = LinearStack(dls, groups=[[0, 1], [2], [3]])
+    for trial in range(2):
+        xs = [qw.synth_activation(c, 150 + 10 * trial + i) for i, (_, c) in enumerate(shapes)]
+        xs[1] = xs[0]  # the fused group reads its first layer's input
+        out = st.run(np.concatenate(xs)).copy()
+        off = 0
+        for d, L, x in zip(dls, layers, xs):
+            y = out[off:off + L.cfg.rows]
+            off += L.cfg.rows
+            assert np.array_equal(y, d.matvec(torch.from_numpy(x).cuda()).cpu().numpy())
