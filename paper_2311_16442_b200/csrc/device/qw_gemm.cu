@@ -525,6 +525,8 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
   p.stages = G.T2 / 2;                               // MMA sub-stages per row
   p.wstages = (p.stages + kSubPerW - 1) / kSubPerW;  // weight stages per row
   p.ks = std::max<uint32_t>(1, std::min<uint32_t>(std::min<uint32_t>(p.wstages, 8u), (uint32_t)num_sms / p.tiles));
+  if (const char* e = std::getenv("QW_GEMM_KS"))  // diagnostics: force the K split
+    p.ks = std::max<uint32_t>(1, std::min<uint32_t>(std::min<uint32_t>(p.wstages, 8u), (uint32_t)std::atoi(e)));
   // A = w 2^-P in fp16: scale2 2^(12-P) <= 2^15 and s4 2^(9-P) <= 2^15
   int P = -126;
   if (max_scale2 > 0.0f && std::isfinite(max_scale2)) P = std::max(P, std::ilogb(max_scale2) - 2);
