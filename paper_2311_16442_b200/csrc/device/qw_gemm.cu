@@ -115,15 +115,17 @@ __device__ __forceinline__ void csr_row(const float* __restrict__ xn, const uint
   if (row >= rows) return;
   const uint32_t e0 = __ldg(row_ptr + row), e1 = __ldg(row_ptr + row + 1);
   float acc = 0.0f;
-  for (uint32_t e = e0; e < e1; e += 8) {
-    float p[8];
+  // 32 entries per round: a row of <= 32 outliers costs two dependent loads
+  for (uint32_t e = e0; e < e1; e += 32) {
+    uint32_t ent[32];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t ent = e + u < e1 ? __ldg(csr + e + u) : 0u;
-      p[u] = __fmul_rn(half_bits_to_float(ent >> 16), __ldg(xn + (ent & 0xFFFFu)));  // original channel (repack)
-    }
+    for (int u = 0; u < 32; ++u) ent[u] = e + u < e1 ? __ldg(csr + e + u) : 0u;
+    float p[32];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < 32; ++u)
+      p[u] = __fmul_rn(half_bits_to_float(ent[u] >> 16), __ldg(xn + (ent[u] & 0xFFFFu)));  // original channel
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
       if (e + u < e1) acc = __fadd_rn(acc, p[u]);
   }
   yn[row] = acc;
@@ -146,6 +148,20 @@ __global__ void __launch_bounds__(kPrepThreads) xprep_kernel(const float* __rest
   const uint32_t n = blockIdx.y;
   const float* xn = x + (size_t)n * G.cols;
   __shared__ float red[kPrepThreads / 32];
+  const uint32_t n2 = G.cols - G.n4;
+  // the gathered elements are loaded before / beside the max pass (only the
+  // scale depends on the max): two dependent loads per thread in total
+  float xv[kPrepPer];
+#pragma unroll
+  for (uint32_t u = 0; u < kPrepPer; ++u) {
+    const uint32_t i = (blockIdx.x * kPrepPer + u) * kPrepThreads + threadIdx.x;
+    xv[u] = 0.0f;
+    if (i < stages * kStageK && n < batch) {
+      const uint32_t st = i / kStageK, k = i % kStageK;
+      const uint32_t slot = k < 96 ? 96 * st + k : G.n2p + 32 * st + (k - 96);
+      if (!(slot >= n2 && slot < G.n2p)) xv[u] = __ldg(xn + __ldg(perm + slot));
+    }
+  }
   float m = 0.0f;
   if (n < batch) {
     const uint32_t n4v = G.cols >> 2;  // cols % 16 == 0 (validate_layer)
@@ -164,7 +180,6 @@ __global__ void __launch_bounds__(kPrepThreads) xprep_kernel(const float* __rest
   const int eb = (int)((__float_as_uint(m) >> 23) & 0xFFu);
   const int e = (eb == 0 ? -126 : eb - 127) - 14;  // max |x'| in [2^14, 2^15)
   if (threadIdx.x == 0 && blockIdx.x == 0) xexp[n] = e;
-  const uint32_t n2 = G.cols - G.n4;
   const int ea = max(-126, min(127, -e));
   const float f1 = p2(ea), f2 = p2(-e - ea);
 #pragma unroll
@@ -172,9 +187,7 @@ __global__ void __launch_bounds__(kPrepThreads) xprep_kernel(const float* __rest
     const uint32_t i = (blockIdx.x * kPrepPer + u) * kPrepThreads + threadIdx.x;
     if (i >= stages * kStageK) break;
     const uint32_t st = i / kStageK, k = i % kStageK;
-    const uint32_t slot = k < 96 ? 96 * st + k : G.n2p + 32 * st + (k - 96);
-    float v = 0.0f;
-    if (n < batch && !(slot >= n2 && slot < G.n2p)) v = __ldg(xn + perm[slot]) * f1 * f2;
+    const float v = xv[u] * f1 * f2;
     const uint32_t off = (k % 8) * 2 + (n % 8) * 16 + (n / 8) * 128 + (k / 8) * 256;
     xpt[(size_t)st * (kBStageBytes / 2) + off / 2] = __half_as_ushort(__float2half_rn(v));
   }

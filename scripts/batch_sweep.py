@@ -1,6 +1,6 @@
 """BASELINE config 3: Llama-2-7B shapes, batch 1/2/4/8/16 (K2 for b = 1, K4 for b >= 2).
 Per-call time from a CUDA-graph chain of N distinct layer copies (inputs > L2).
-usage: python scripts/batch_sweep.py [N]  -> one JSON line per (shape, batch)"""
+usage: python scripts/batch_sweep.py [N] [nopdl]  -> one JSON line per (shape, batch)"""
 import json
 import sys
 from pathlib import Path
@@ -12,6 +12,7 @@ import torch  # noqa: E402
 import paper_2311_16442_b200 as qw  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+PDL = not (len(sys.argv) > 2 and sys.argv[2] == "nopdl")
 out = []
 for name, rows, cols in (("q_proj", 4096, 4096), ("gate_proj", 11008, 4096), ("down_proj", 4096, 11008)):
     layer = qw.synth_layer(rows, cols, seed=7)
@@ -24,7 +25,7 @@ for name, rows, cols in (("q_proj", 4096, 4096), ("gate_proj", 11008, 4096), ("d
 
         def run():
             for i, d in enumerate(dls):
-                d.matvec(xs, out=ys[i], pdl=(b == 1))
+                d.matvec(xs, out=ys[i], pdl=PDL)
         run()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
