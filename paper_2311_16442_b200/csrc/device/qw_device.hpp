@@ -81,7 +81,8 @@ struct GemmPlan {
   alignas(64) uint8_t tmap[5][128];  // CUtensorMap: code2, meta, code4, s4, z4 boxes
   alignas(64) uint8_t tmap_so[128];  // CUtensorMap: sorder box of a tile's row blocks
   uint32_t so_rows = 0;
-  float* partial = nullptr;  // [ks][16][rows] split-K partial sums
+  uint32_t stream = 0, W = 0, C = 0, kmax = 0;  // stream-K: W weight stages over C CTAs, kmax partial slots per tile
+  float* partial = nullptr;  // [tiles][kmax][128][16] stream-K partial sums
   uint32_t* counters = nullptr;  // [tiles] split-K arrivals (self-resetting)
   uint16_t* xpt = nullptr;   // [stages][128 k][16 n] fp16 B tiles (UMMA K-major layout)
   int* xexp = nullptr;       // [16] per-column power-of-two exponents

@@ -23,9 +23,16 @@
 //                 issues 8 tcgen05.mma per stage, tcgen05.commit frees the A/B
 //                 buffers.  Warps 2-5 read the 128x16 accumulator with
 //                 tcgen05.ld, undo the power-of-two scales, add the CSR
-//                 outliers (exact fp32) and store y -- or, with K splits, park
-//                 partials; the last CTA of a tile sums them in split order
-//                 (deterministic).
+//                 outliers (exact fp32) and store y.  Two K-split schedules:
+//                 cluster split-K (the tile's splits form a cluster and sum
+//                 through distributed shared memory in split order) and
+//                 stream-K (gemm_kernel<true>: 148 CTAs take equal contiguous
+//                 ranges of the tiles x weight-stages work, at most two tiles
+//                 each with one TMEM accumulator per tile; partials go to
+//                 global slots and a tile's last arrival sums them in
+//                 contributor order).  Both deterministic; plan_gemm picks
+//                 stream-K when it shortens the critical path (86-tile
+//                 gate/up: every SM busy instead of 86).
 //
 // A tile value = RN_fp16((c - z) * (eff - zero2) * scale2 * 2^-P): the
 // integer part is formed exactly by one HFMA2 on subnormal-coded operands
@@ -211,6 +218,7 @@ struct GemmArgs {
   const float* ycsr;  // [batch][rows] CSR outlier sums (prologue kernel)
   uint32_t* counters;
   uint32_t batch, ks, stages, wstages;
+  uint32_t stream, W, C, kmax;  // stream-K: W = tiles x wstages over C CTAs; kmax partial slots per tile
   int shift;
   uint32_t rb_magic, rb_one;
   unsigned long long* dbg;  // optional [grid][8] %globaltimer stamps
@@ -223,6 +231,15 @@ __device__ __forceinline__ void gstamp(const GemmArgs& a, uint32_t ev) {
   }
 }
 
+// stream-K: the CTA whose weight-stage range holds flattened index i
+// (ranges [c W / C, (c + 1) W / C)): the largest c with floor(c W / C) <= i
+__device__ __forceinline__ uint32_t stream_first(const GemmArgs& a, uint32_t i) {
+  return (uint32_t)(((uint64_t)(i + 1) * a.C - 1) / a.W);
+}
+
+// kStream: stream-K schedule (a separate instantiation: the cluster split-K
+// kernel keeps its tighter hot loop)
+template <bool kStream>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -243,15 +260,35 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   // [128][kDenseStride]: 16-byte rows so the split-K reduction reads float4s
   float* s_dense = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_last + 3) + 15) & ~uintptr_t(15));
 
-  const uint32_t tile = blockIdx.x / a.ks, split = blockIdx.x % a.ks;
-  // K split over weight stages (8 tiles); sub-stages of 2 tiles feed the MMA
-  const uint32_t w0 = (uint32_t)((uint64_t)split * a.wstages / a.ks);
-  const uint32_t w1 = (uint32_t)((uint64_t)(split + 1) * a.wstages / a.ks);
-  const uint32_t nw = w1 - w0;
-  const uint32_t u0 = w0 * kSubPerW, u1 = min(w1 * kSubPerW, a.stages);
-  const uint32_t nsub = u1 - u0;  // sub-stages of this CTA
+  // Work: up to two segments (tile, weight-stage range).  Cluster split-K
+  // (kStream false): CTA = (tile, split), one segment.  Stream-K: the
+  // tiles x wstages weight stages are cut into C equal contiguous ranges (one
+  // CTA each, every SM busy); a range spans at most two tiles (W / C <=
+  // wstages), partials meet in global memory (stream_fixup).
+  // (scalars, not arrays: dynamic indexing would put them on the stack)
+  uint32_t tile, tile1, w00, nw0, nw1;
+  const uint32_t split = kStream ? 0u : blockIdx.x % a.ks;
+  if (kStream) {
+    const uint32_t i0 = (uint32_t)((uint64_t)blockIdx.x * a.W / a.C);
+    const uint32_t i1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * a.W / a.C);
+    tile = i0 / a.wstages, w00 = i0 % a.wstages;
+    const uint32_t e0 = min(i1, (tile + 1) * a.wstages);
+    nw0 = e0 - i0, tile1 = tile + 1, nw1 = i1 - e0;
+  } else {
+    // K split over weight stages (8 tiles); sub-stages of 2 tiles feed the MMA
+    const uint32_t w0 = (uint32_t)((uint64_t)split * a.wstages / a.ks);
+    const uint32_t w1 = (uint32_t)((uint64_t)(split + 1) * a.wstages / a.ks);
+    tile = tile1 = blockIdx.x / a.ks, w00 = w0, nw0 = w1 - w0, nw1 = 0;
+  }
+  const uint32_t nseg = (kStream && nw1) ? 2u : 1u;
+  const uint32_t nw = nw0 + nw1;
+  // sub-stages of this CTA (stream-K needs stages % kSubPerW == 0)
+  const uint32_t nsub = kStream ? nw * kSubPerW : min((w00 + nw) * kSubPerW, a.stages) - w00 * kSubPerW;
+  const uint32_t seg1_sub = nw0 * kSubPerW;  // first sub-stage of segment 1
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  const uint32_t rb_tile = a.rb_one ? tile * kTileRows : __umulhi(tile * kTileRows, a.rb_magic);
+  auto rb_of = [&](uint32_t t) { return a.rb_one ? t * kTileRows : __umulhi(t * kTileRows, a.rb_magic); };
+  // local weight stage j -> weight stage within its segment's tile
+  auto wst_of = [&](uint32_t j) { return (!kStream || j < nw0) ? w00 + j : j - nw0; };
 
   if (threadIdx.x == 0) {
     for (uint32_t i = 0; i < kWSlots; ++i) mbar_init(&wfull[i], 1), mbar_init(&wempty[i], kDqWarps);
@@ -273,9 +310,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 0) {
     // ---------------- producer: weight boxes (8 tiles) + B tiles (per sub-stage)
     if (lane == 0) {
-      const int qy = (int)(tile * kTileQuads);
       auto load_w = [&](uint32_t i) {
-        const uint32_t wst = w0 + i, ws = i % kWSlots;
+        const uint32_t t = (!kStream || i < nw0) ? tile : tile1;
+        const int qy = (int)(t * kTileQuads);
+        const uint32_t wst = wst_of(i), ws = i % kWSlots;
         if (i >= kWSlots) mbar_wait(&wempty[ws], ((i / kWSlots) - 1) & 1u);
         uint8_t* dst = sW + ws * kWStageBytes;
         mbar_expect_tx(&wfull[ws], kOffSo + a.so_rows * kSoBoxG * 4);
@@ -284,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         tma_load_2d(dst + kOffC4, &a.tm[2], (int)(G.off_c4 / 4 + 64 * wst), qy, &wfull[ws]);
         tma_load_2d(dst + kOffS4, &a.tm[3], (int)(G.off_s4 / 4 + 16 * wst), qy, &wfull[ws]);
         tma_load_2d(dst + kOffZ4, &a.tm[4], (int)(G.off_z4 / 4 + 4 * wst), qy, &wfull[ws]);
-        tma_load_2d(dst + kOffSo, &a.tso, (int)(24 * wst), (int)rb_tile, &wfull[ws]);
+        tma_load_2d(dst + kOffSo, &a.tso, (int)(24 * wst), (int)rb_of(t), &wfull[ws]);
       };
       const uint32_t wpre = min(nw, kWSlots);
       for (uint32_t i = 0; i < wpre; ++i) load_w(i);  // the weights do not depend on x
@@ -294,7 +332,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const uint32_t bs = i % kBSlots;
         if (i >= kBSlots) mbar_wait(&bempty[bs], ((i / kBSlots) - 1) & 1u);
         mbar_expect_tx(&bfull[bs], kBStageBytes);
-        bulk_load_nohint(sB + bs * kBStageBytes, a.xpt + (size_t)(u0 + i) * (kBStageBytes / 2), kBStageBytes,
+        const uint32_t u = wst_of(i / kSubPerW) * kSubPerW + i % kSubPerW;  // sub-stage within the tile's K
+        bulk_load_nohint(sB + bs * kBStageBytes, a.xpt + (size_t)u * (kBStageBytes / 2), kBStageBytes,
                          &bfull[bs]);
         if ((i % kSubPerW) == 0 && wnext < nw) load_w(wnext++);
       }
@@ -310,13 +349,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t abase = smem_addr(sA + ab * kATileBytes), bbase = smem_addr(sB + bs * kBStageBytes);
+        // segment s accumulates in TMEM columns [16 s, 16 s + 16)
+        const uint32_t first = (i == 0 || (kStream && i == seg1_sub)) ? 1u : 0u;
+        const uint32_t dacc = tmem + ((kStream && i >= seg1_sub) ? 16u : 0u);
 #pragma unroll
         for (uint32_t kk = 0; kk < kStageK / 16; ++kk) {
           const uint64_t da = umma_desc(abase + 2 * kk * kALbo, kALbo, kASbo);
           const uint64_t db = umma_desc(bbase + kk * 512, 256, 128);
-          const uint32_t acc = (i | kk) ? 1u : 0u;
+          const uint32_t acc = (first && kk == 0) ? 0u : 1u;
           asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
-                       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(tmem),
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(dacc),
                        "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -333,9 +375,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     // ones, so no warp diverges over the two decode paths.
     const uint32_t dw = warp - 2, q = lane;
     const uint32_t j = dw < 12 ? dw >> 1 : 6 + ((dw - 12) >> 1), h = dw & 1u;
-    const uint32_t quad = tile * kTileQuads + q;
-    const uint32_t row0 = min(quad * 4, G.rows - 1);
-    const uint32_t rb_local = (a.rb_one ? row0 : __umulhi(row0, a.rb_magic)) - rb_tile;
+    // the quad's row block relative to its tile's first, per segment
+    auto rbl_of = [&](uint32_t t) {
+      const uint32_t row0 = min((t * kTileQuads + q) * 4, G.rows - 1);
+      return (a.rb_one ? row0 : __umulhi(row0, a.rb_magic)) - rb_of(t);
+    };
+    const uint32_t rbl0 = rbl_of(tile), rbl1 = kStream ? rbl_of(tile1) : rbl0;
     const float s2sc = p2(12 - a.shift), s4sc = p2(9 - a.shift);
     const uint32_t sub = j % 3;
     const uint32_t esh = sub == 0 ? 6u : (sub == 1 ? 10u : 13u), emask = sub == 0 ? 15u : 7u;
@@ -349,6 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       if (s4i == 0) mbar_wait(&wfull[ws], (wi / kWSlots) & 1u);
       if (threadIdx.x == 64 && i == 3) gstamp(a, 1);  // sub-stage 3 weights present
       const uint8_t* w = sW + ws * kWStageBytes;
+      const uint32_t rb_local = (!kStream || wi < nw0) ? rbl0 : rbl1;
       uint32_t out[8][2];
       if (j < 6) {
         const uint32_t g6 = 6 * s4i + j;  // 2-bit group within the weight stage
@@ -433,23 +479,74 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       if (threadIdx.x == 64) gstamp(a, 7);  // accumulator ready
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t quarter = warp & 3u;
-      uint32_t r[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(tmem + ((quarter * 32u) << 16)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;");
       const uint32_t t = quarter * 32 + lane;  // row within the tile
+      for (uint32_t sg = 0; sg < nseg; ++sg) {
+        uint32_t r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(tmem + 16u * sg + ((quarter * 32u) << 16)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        float v[16];
 #pragma unroll
-      for (int n = 0; n < 16; ++n) s_dense[t * kDenseStride + n] = __uint_as_float(r[n]) * csc[n];
+        for (int n = 0; n < 16; ++n) v[n] = __uint_as_float(r[n]) * csc[n];
+        if (!kStream) {
+#pragma unroll
+          for (int n = 0; n < 16; ++n) s_dense[t * kDenseStride + n] = v[n];
+          continue;
+        }
+        const uint32_t st = sg ? tile1 : tile, row = st * kTileRows + t;
+        const uint32_t cf = stream_first(a, st * a.wstages), nc = stream_first(a, st * a.wstages + a.wstages - 1) + 1 - cf;
+        if (nc == 1) {  // the whole tile's K is ours: finish the rows here
+          if (row < G.rows) {
+#pragma unroll
+            for (uint32_t n = 0; n < 16; ++n)
+              if (n < a.batch) a.y[(size_t)n * G.rows + row] = v[n] + __ldg(a.ycsr + (size_t)n * G.rows + row);
+          }
+        } else {  // partial slot (tile, contributor index)
+          float4* dst = reinterpret_cast<float4*>(a.partial + ((size_t)(st * a.kmax + blockIdx.x - cf) * kTileRows + t) * 16);
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) dst[c4] = make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+        }
+      }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) gstamp(a, 2);  // CTA joined after the accumulator read
 
-  // dense part of this split is in s_dense[row][n] (row-major, padded stride)
-  if (a.ks == 1) {
+  if (kStream) {
+    // stream-K fixup: the last contributor of a tile (arrival counter) sums
+    // the tile's partial slots in contributor order -- deterministic
+    pdl_wait();  // the CSR sums are the prologue kernel's
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (uint32_t sg = 0; sg < 2; ++sg) {
+        s_last[sg] = 0;
+        if (sg >= nseg) continue;
+        const uint32_t st = sg ? tile1 : tile;
+        const uint32_t cf = stream_first(a, st * a.wstages), nc = stream_first(a, st * a.wstages + a.wstages - 1) + 1 - cf;
+        if (nc > 1 && atomicAdd(a.counters + st, 1u) == nc - 1) s_last[sg] = nc;
+      }
+    }
+    __syncthreads();
+    for (uint32_t sg = 0; sg < nseg; ++sg) {
+      const uint32_t nc = s_last[sg];
+      if (!nc) continue;
+      __threadfence();
+      const uint32_t st = sg ? tile1 : tile;
+      const float* part = a.partial + (size_t)st * a.kmax * kTileRows * 16;
+      for (uint32_t i = threadIdx.x; i < kTileRows * a.batch; i += blockDim.x) {
+        const uint32_t t = i % kTileRows, n = i / kTileRows, row = st * kTileRows + t;
+        float sum = __ldcg(part + t * 16 + n);
+        for (uint32_t k = 1; k < nc; ++k) sum += __ldcg(part + ((size_t)k * kTileRows + t) * 16 + n);
+        if (row < G.rows) a.y[(size_t)n * G.rows + row] = sum + __ldg(a.ycsr + (size_t)n * G.rows + row);
+      }
+      if (threadIdx.x == 0) a.counters[st] = 0;  // every contributor has arrived: reset for the next call
+    }
+  } else if (a.ks == 1) {
+    // dense part of this split is in s_dense[row][n] (row-major, padded stride)
     // the dense sum, then the outliers (row_fma, engine.cpp:111-122): their
     // per-row CSR sums (exact fp32, CSR order) come from the prologue kernel
     pdl_wait();
@@ -538,8 +635,23 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
   p.stages = G.T2 / 2;                               // MMA sub-stages per row
   p.wstages = (p.stages + kSubPerW - 1) / kSubPerW;  // weight stages per row
   p.ks = std::max<uint32_t>(1, std::min<uint32_t>(std::min<uint32_t>(p.wstages, 8u), (uint32_t)num_sms / p.tiles));
-  if (const char* e = std::getenv("QW_GEMM_KS"))  // diagnostics: force the K split
-    p.ks = std::max<uint32_t>(1, std::min<uint32_t>(std::min<uint32_t>(p.wstages, 8u), (uint32_t)std::atoi(e)));
+  const char* force_ks = std::getenv("QW_GEMM_KS");  // diagnostics: force the cluster K split
+  if (force_ks)
+    p.ks = std::max<uint32_t>(1, std::min<uint32_t>(std::min<uint32_t>(p.wstages, 8u), (uint32_t)std::atoi(force_ks)));
+  // stream-K when it shortens the critical path: every SM takes an equal
+  // contiguous range of the tiles x wstages weight stages (cluster split-K
+  // leaves SMs idle when 148 / tiles is small, e.g. 86 tiles -> ks = 1)
+  {
+    const uint32_t W = p.tiles * p.wstages, C = std::min<uint32_t>((uint32_t)num_sms, W);
+    const uint32_t crit_ks = (p.wstages + p.ks - 1) / p.ks, crit_stream = (W + C - 1) / C;
+    if (!force_ks && !std::getenv("QW_GEMM_NOSTREAM") && p.stages % kSubPerW == 0 && p.tiles <= C &&
+        crit_stream < crit_ks) {
+      p.stream = 1, p.W = W, p.C = C, p.ks = 1;
+      auto first = [&](uint64_t i) { return (uint32_t)(((i + 1) * C - 1) / W); };
+      for (uint32_t t = 0; t < p.tiles; ++t)
+        p.kmax = std::max(p.kmax, first((uint64_t)t * p.wstages + p.wstages - 1) + 1 - first((uint64_t)t * p.wstages));
+    }
+  }
   // A = w 2^-P in fp16: scale2 2^(12-P) <= 2^15 and s4 2^(9-P) <= 2^15
   int P = -126;
   if (max_scale2 > 0.0f && std::isfinite(max_scale2)) P = std::max(P, std::ilogb(max_scale2) - 2);
@@ -569,7 +681,9 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
     if (r != CUDA_SUCCESS) return 0;
   }
   cudaError_t e;
-  if ((e = cudaMalloc((void**)&p.partial, (size_t)p.ks * 16 * G.rows * 4 + 16)) != cudaSuccess) return (int)e;
+  // stream-K partial slots [tiles][kmax][128 rows][16 columns]
+  if ((e = cudaMalloc((void**)&p.partial, (size_t)p.tiles * std::max(p.kmax, 1u) * kTileRows * 16 * 4)) != cudaSuccess)
+    return (int)e;
   if ((e = cudaMalloc((void**)&p.counters, (size_t)p.tiles * 4)) != cudaSuccess) return (int)e;
   if ((e = cudaMemset(p.counters, 0, (size_t)p.tiles * 4)) != cudaSuccess) return (int)e;
   if ((e = cudaMalloc((void**)&p.xpt, (size_t)p.stages * kBStageBytes)) != cudaSuccess) return (int)e;
@@ -577,11 +691,12 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
   if ((e = cudaMalloc((void**)&p.ycsr, (size_t)16 * G.rows * 4)) != cudaSuccess) return (int)e;
   static bool attr = false;
   if (!attr) {
-    if ((e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem)) !=
-        cudaSuccess)
-      return (int)e;
-    if ((e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
-      return (int)e;
+    for (const void* k : {(const void*)gemm_kernel<false>, (const void*)gemm_kernel<true>}) {
+      if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem)) != cudaSuccess)
+        return (int)e;
+      if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+        return (int)e;
+    }
     attr = true;
   }
   p.ok = 1;
@@ -615,12 +730,13 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   a.xpt = p.xpt, a.xexp = p.xexp, a.x = x, a.y = y;
   a.partial = p.partial, a.counters = p.counters, a.ycsr = p.ycsr;
   a.batch = batch, a.ks = p.ks, a.stages = p.stages, a.wstages = p.wstages, a.shift = p.shift;
+  a.stream = p.stream, a.W = p.W, a.C = p.C, a.kmax = p.kmax;
   a.rb_magic = L.plan.rb_magic, a.rb_one = L.plan.rb_one;
   a.dbg = dbg;
   // cluster = the tile's K splits (DSMEM reduction); PDL: the weight stream
   // starts while the prologue runs, B tiles / scales wait for it
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.tiles * p.ks);
+  cfg.gridDim = dim3(p.stream ? p.C : p.tiles * p.ks);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kGemmSmem;
   cfg.stream = st;
@@ -633,7 +749,8 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   static const bool no_pdl = std::getenv("QW_GEMM_NOPDL") != nullptr;  // diagnostics
   cfg.numAttrs = no_pdl ? 1 : 2;
   void* params[] = {&a};
-  return (int)cudaLaunchKernelExC(&cfg, (const void*)gemm_kernel, params);
+  return (int)cudaLaunchKernelExC(&cfg, p.stream ? (const void*)gemm_kernel<true> : (const void*)gemm_kernel<false>,
+                                  params);
 }
 
 }  // namespace qwdev

@@ -186,6 +186,9 @@ BATCH_GEOMS = [
     (130, 768, 16),     # rows % 4 != 0 inside the last tile, full batch
     (512, 4096, 8),     # K split across CTAs (split-K fixup)
     (4096, 4096, 16),   # Llama-2-7B q_proj, batch 16
+    (10240, 2048, 3),   # stream-K: 80 tiles x 4 weight stages over 148 CTAs (two-tile ranges)
+    (11008, 4096, 4),   # Llama-2-7B gate_proj: stream-K, 86 tiles
+    (8192, 8192, 16),   # Llama-2-70B q_proj: stream-K, 64 tiles x 16 weight stages
 ]
 
 
