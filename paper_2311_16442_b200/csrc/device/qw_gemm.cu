@@ -77,6 +77,7 @@ constexpr uint32_t kOffC2 = 0, kOffMeta = kOffC2 + 32 * kBoxC2 * 4, kOffC4 = kOf
                    kWStageBytes = (kOffSo + kSoRowsMax * kSoBoxG * 4 + 1023) / 1024 * 1024;  // 28 KB
 constexpr uint32_t kWSlots = 2, kBSlots = 8, kABufs = 3;
 constexpr uint32_t kDqWarps = 16;
+constexpr uint32_t kStreamMaxBatch = 8;  // stream-K above this batch measured slower (launch_gemm)
 constexpr uint32_t kDenseStride = 20;  // fp32 words per accumulator row in shared memory
 constexpr uint32_t kThreads = (2 + kDqWarps) * 32;
 
@@ -646,7 +647,7 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
     const uint32_t crit_ks = (p.wstages + p.ks - 1) / p.ks, crit_stream = (W + C - 1) / C;
     if (!force_ks && !std::getenv("QW_GEMM_NOSTREAM") && p.stages % kSubPerW == 0 && p.tiles <= C &&
         crit_stream < crit_ks) {
-      p.stream = 1, p.W = W, p.C = C, p.ks = 1;
+      p.stream = 1, p.W = W, p.C = C;
       auto first = [&](uint64_t i) { return (uint32_t)(((i + 1) * C - 1) / W); };
       for (uint32_t t = 0; t < p.tiles; ++t)
         p.kmax = std::max(p.kmax, first((uint64_t)t * p.wstages + p.wstages - 1) + 1 - first((uint64_t)t * p.wstages));
@@ -736,20 +737,25 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   // cluster = the tile's K splits (DSMEM reduction); PDL: the weight stream
   // starts while the prologue runs, B tiles / scales wait for it
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.stream ? p.C : p.tiles * p.ks);
+  // stream-K only up to batch 8: its global partial round trip grows with the
+  // batch (gate_proj b = 16: 40.8 vs 40.4 us with cluster split-K)
+  const bool use_stream = p.stream && batch <= kStreamMaxBatch;
+  a.stream = use_stream;
+  a.ks = use_stream ? 1u : p.ks;
+  cfg.gridDim = dim3(use_stream ? p.C : p.tiles * p.ks);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kGemmSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.ks, attr[0].val.clusterDim.y = 1, attr[0].val.clusterDim.z = 1;
+  attr[0].val.clusterDim.x = a.ks, attr[0].val.clusterDim.y = 1, attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   static const bool no_pdl = std::getenv("QW_GEMM_NOPDL") != nullptr;  // diagnostics
   cfg.numAttrs = no_pdl ? 1 : 2;
   void* params[] = {&a};
-  return (int)cudaLaunchKernelExC(&cfg, p.stream ? (const void*)gemm_kernel<true> : (const void*)gemm_kernel<false>,
+  return (int)cudaLaunchKernelExC(&cfg, use_stream ? (const void*)gemm_kernel<true> : (const void*)gemm_kernel<false>,
                                   params);
 }
 
