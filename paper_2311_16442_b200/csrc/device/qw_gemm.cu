@@ -683,7 +683,8 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
   }
   cudaError_t e;
   // stream-K partial slots [tiles][kmax][128 rows][16 columns]
-  if ((e = cudaMalloc((void**)&p.partial, (size_t)p.tiles * std::max(p.kmax, 1u) * kTileRows * 16 * 4)) != cudaSuccess)
+  if ((e = cudaMalloc((void**)&p.partial, p.stream ? (size_t)p.tiles * p.kmax * kTileRows * 16 * 4 : 16)) !=
+      cudaSuccess)
     return (int)e;
   if ((e = cudaMalloc((void**)&p.counters, (size_t)p.tiles * 4)) != cudaSuccess) return (int)e;
   if ((e = cudaMemset(p.counters, 0, (size_t)p.tiles * 4)) != cudaSuccess) return (int)e;
