@@ -108,7 +108,7 @@ __device__ __forceinline__ float p2(int e) { return __uint_as_float((uint32_t)(m
 // holds 2-bit permuted channels [96 st, 96 st + 96) then 4-bit channels
 // n2p + [32 st, 32 st + 32); element (k, n) of a stage at
 // (k % 8) * 2 + (n % 8) * 16 + (n / 8) * 128 + (k / 8) * 256.
-// Grid (chunks + csr_blocks, 16): a chunk CTA re-derives its column's
+// Grid (chunks + csr_blocks, batch): a chunk CTA re-derives its column's
 // power-of-two scale from a full (L2-resident, independent-load) max, then
 // converts kPrepPer elements per thread (independent loads, so no thread waits
 // on a chain); few enough CTAs to run in one wave beside the GEMM's.
@@ -719,7 +719,10 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   cudaStream_t st = (cudaStream_t)stream;
   const uint32_t chunks = (p.stages * kStageK + kPrepThreads * kPrepPer - 1) / (kPrepThreads * kPrepPer);
   const uint32_t csr_blocks = (G.rows + kPrepThreads - 1) / kPrepThreads;
-  xprep_kernel<<<dim3(chunks + csr_blocks, 16), kPrepThreads, 0, st>>>(x, L.perm16, G, p.stages, batch, p.xpt,
+  // one grid row per live column: the B columns >= batch are never stored
+  // (MMA columns are independent), and a small prologue grid leaves the SMs
+  // free for the GEMM's CTAs, which launch as soon as it starts (PDL)
+  xprep_kernel<<<dim3(chunks + csr_blocks, batch), kPrepThreads, 0, st>>>(x, L.perm16, G, p.stages, batch, p.xpt,
                                                                        p.xexp, chunks, L.row_ptr, L.csr, p.ycsr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
