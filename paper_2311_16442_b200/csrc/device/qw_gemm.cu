@@ -77,7 +77,7 @@ constexpr uint32_t kOffC2 = 0, kOffMeta = kOffC2 + 32 * kBoxC2 * 4, kOffC4 = kOf
                    kWStageBytes = (kOffSo + kSoRowsMax * kSoBoxG * 4 + 1023) / 1024 * 1024;  // 28 KB
 constexpr uint32_t kWSlots = 2, kBSlots = 8, kABufs = 3;
 constexpr uint32_t kDqWarps = 16;
-constexpr uint32_t kStreamMaxBatch = 8;  // stream-K above this batch measured slower (launch_gemm)
+constexpr uint32_t kStreamMaxK = 8;       // stream-K: contributors per tile (partial slots) at most
 constexpr uint32_t kDenseStride = 20;  // fp32 words per accumulator row in shared memory
 constexpr uint32_t kThreads = (2 + kDqWarps) * 32;
 
@@ -540,8 +540,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const float* part = a.partial + (size_t)st * a.kmax * kTileRows * 16;
       for (uint32_t i = threadIdx.x; i < kTileRows * a.batch; i += blockDim.x) {
         const uint32_t t = i % kTileRows, n = i / kTileRows, row = st * kTileRows + t;
-        float sum = __ldcg(part + t * 16 + n);
-        for (uint32_t k = 1; k < nc; ++k) sum += __ldcg(part + ((size_t)k * kTileRows + t) * 16 + n);
+        float v[kStreamMaxK];  // all slots in flight, then summed in contributor order
+#pragma unroll
+        for (uint32_t k = 0; k < kStreamMaxK; ++k)
+          v[k] = k < nc ? __ldcg(part + ((size_t)k * kTileRows + t) * 16 + n) : 0.0f;
+        float sum = v[0];
+#pragma unroll
+        for (uint32_t k = 1; k < kStreamMaxK; ++k)
+          if (k < nc) sum += v[k];
         if (row < G.rows) a.y[(size_t)n * G.rows + row] = sum + __ldg(a.ycsr + (size_t)n * G.rows + row);
       }
       if (threadIdx.x == 0) a.counters[st] = 0;  // every contributor has arrived: reset for the next call
@@ -647,10 +653,11 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
     const uint32_t crit_ks = (p.wstages + p.ks - 1) / p.ks, crit_stream = (W + C - 1) / C;
     if (!force_ks && !std::getenv("QW_GEMM_NOSTREAM") && p.stages % kSubPerW == 0 && p.tiles <= C &&
         crit_stream < crit_ks) {
-      p.stream = 1, p.W = W, p.C = C;
       auto first = [&](uint64_t i) { return (uint32_t)(((i + 1) * C - 1) / W); };
+      uint32_t kmax = 0;
       for (uint32_t t = 0; t < p.tiles; ++t)
-        p.kmax = std::max(p.kmax, first((uint64_t)t * p.wstages + p.wstages - 1) + 1 - first((uint64_t)t * p.wstages));
+        kmax = std::max(kmax, first((uint64_t)t * p.wstages + p.wstages - 1) + 1 - first((uint64_t)t * p.wstages));
+      if (kmax <= kStreamMaxK) p.stream = 1, p.W = W, p.C = C, p.kmax = kmax;
     }
   }
   // A = w 2^-P in fp16: scale2 2^(12-P) <= 2^15 and s4 2^(9-P) <= 2^15
@@ -741,9 +748,7 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   // cluster = the tile's K splits (DSMEM reduction); PDL: the weight stream
   // starts while the prologue runs, B tiles / scales wait for it
   cudaLaunchConfig_t cfg = {};
-  // stream-K only up to batch 8: its global partial round trip grows with the
-  // batch (gate_proj b = 16: 40.8 vs 40.4 us with cluster split-K)
-  const bool use_stream = p.stream && batch <= kStreamMaxBatch;
+  const bool use_stream = p.stream != 0;
   a.stream = use_stream;
   a.ks = use_stream ? 1u : p.ks;
   cfg.gridDim = dim3(use_stream ? p.C : p.tiles * p.ks);

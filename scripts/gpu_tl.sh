@@ -1,7 +1,9 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "batched or large_activation or geometries or zero" 2>&1 | tail -2
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "batched" 2>&1 | tail -2
+for v in stream nostream; do echo "== $v"
+if [ $v = stream ]; then unset QW_GEMM_NOSTREAM; else export QW_GEMM_NOSTREAM=1; fi
 timeout 600 python scripts/batch_sweep.py 24 2>/dev/null | python -c "
 import json,sys
 for l in sys.stdin:
     d=json.loads(l)
-    if d['batch'] > 1: print(d['shape'], d['batch'], d['us_per_call'])"
+    if d['batch'] > 1 and True: print(d['shape'], d['batch'], d['us_per_call'])"; done

@@ -189,7 +189,7 @@ BATCH_GEOMS = [
     (10240, 2048, 3),   # stream-K: 80 tiles x 4 weight stages over 148 CTAs (two-tile ranges)
     (11008, 4096, 4),   # Llama-2-7B gate_proj: stream-K, 86 tiles
     (8192, 8192, 8),    # Llama-2-70B q_proj: stream-K, 64 tiles x 16 weight stages
-    (11008, 4096, 16),  # gate_proj above the stream-K batch limit: cluster split-K
+    (11008, 4096, 16),  # gate_proj, stream-K at the full batch
     (4096, 11008, 2),   # Llama-2-7B down_proj: cluster split-K, 86 sub-stages
 ]
 
