@@ -144,8 +144,11 @@ int qw_synth_activation(uint32_t cols, uint64_t seed, float* out);
 
 /* ------------------------------------------------------- device layer (B200)
  * Upload: validate_layer, repack into the 4-row device records (DESIGN.md
- * "HBM layout"), copy to HBM.  The handle is immutable and may be used
- * concurrently from several streams, each with its own workspace. */
+ * "HBM layout"), copy to HBM.  Batch-1 calls (the fused GEMV) only read the
+ * handle and may run concurrently from several streams.  Batched calls
+ * (batch 2..16, the tcgen05 path) use scratch owned by the layer (B tiles,
+ * CSR sums, stream-K partials and arrival counters): order them on one
+ * stream (or with events) per layer. */
 typedef struct qw_layer qw_layer;
 typedef struct qw_workspace qw_workspace;
 
