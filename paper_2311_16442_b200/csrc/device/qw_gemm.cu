@@ -243,7 +243,9 @@ __device__ __forceinline__ uint32_t stream_first(const GemmArgs& a, uint32_t i) 
 template <bool kStream>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the __shared__ array (an
+  // integer round trip would make every A/W access a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   const Geometry& G = a.g;
   uint8_t* sA = smem;                                // kABufs x kATileBytes
   uint8_t* sB = sA + kABufs * kATileBytes;           // kBSlots x 4 KB
@@ -259,7 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dfull + 1);
   uint32_t* s_last = tmem_slot + 1;
   // [128][kDenseStride]: 16-byte rows so the split-K reduction reads float4s
-  float* s_dense = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_last + 3) + 15) & ~uintptr_t(15));
+  float* s_dense = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s_last + 3) +
+                                            ((16u - (smem_addr(s_last + 3) & 15u)) & 15u));
 
   // Work: up to two segments (tile, weight-stage range).  Cluster split-K
   // (kStream false): CTA = (tile, split), one segment.  Stream-K: the
