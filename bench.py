@@ -17,10 +17,11 @@ cloned device-to-device so each of the 224 GEMVs reads its own HBM copy.
             activations + step + D2H of all outputs, host wall clock
   roofline: the fused GEMV kernel alone on the q/k/v/o shape
   cpu_baseline: the reference's matvec_pipelined (oracle/_ref, all host
-            threads) on one decoder layer's 7 linears (bounded sample)
+            threads) on one decoder layer's 7 linears (bounded sample), plus
+            1-thread matvec_oracle and a thread-scaling self-check
 
 `--impl reference` times the reference CPU implementation (oracle/_ref) on
-the same 7 linears.  Under torchrun every rank runs its own replica of the
+the same 224-GEMV step (layers produced by the reference's own quantizer).  Under torchrun every rank runs its own replica of the
 step (batch-1 decode does not shard without a collective): scaling "weak".
 """
 from __future__ import annotations
@@ -107,10 +108,37 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- layers
+def layer_paths(cache_dir: Path):
+    return [cache_dir / f"{name}.qwl" for name, _, _ in SHAPES_7B]
+
+
+def ref_make_layers(cache_dir: Path):
+    """The 7 distinct linears as reference PackedLayers, produced by the
+    reference's OWN synth + quantize_layer (synth.cpp:11-56,
+    quantizer.cpp:132-146) and cached as QWL1 by its own serializer
+    (container.cpp:321-359).  Only oracle/_ref is called here, so the
+    reference arm never maps this repo's library."""
+    import oracle
+    out = []
+    for i, ((name, rows, cols), path) in enumerate(zip(SHAPES_7B, layer_paths(cache_dir))):
+        if path.exists():
+            out.append(oracle.RefLayer.read(path))
+            continue
+        w = oracle.ref_synth_gaussian(rows, cols, 7 + i)
+        h = oracle.ref_synth_calibration(cols, 7 + i)
+        r = oracle.RefLayer.quantize(w, h, ALPHA, GROUP2, RATIO)
+        r.write(str(path) + ".tmp")
+        os.replace(str(path) + ".tmp", path)
+        out.append(r)
+    return out
+
+
 def make_layers(rank: int, world: int, cache_dir: Path, threads: int):
-    """Quantize the 7 distinct linears once (rank 0), share through QWL1 files."""
+    """The same 7 layers for the GPU arm: read the QWL1 cache if the reference
+    arm (or an earlier run) wrote it, else produce them with this repo's
+    producer -- bit-identical to the reference's (tests/test_producer.py)."""
     import paper_2311_16442_b200 as qw
-    paths = [cache_dir / f"{name}.qwl" for name, _, _ in SHAPES_7B]
+    paths = layer_paths(cache_dir)
     if rank == 0:
         for i, (name, rows, cols) in enumerate(SHAPES_7B):
             if not paths[i].exists():
@@ -125,92 +153,123 @@ def make_layers(rank: int, world: int, cache_dir: Path, threads: int):
 
 
 # --------------------------------------------------------------- CPU legs
-def cpu_reference_sample(layers, budget_s: float, threads: int):
-    """The reference's own matvec_pipelined (or the C port) on the 7 linears."""
+def ref_inputs(refs):
+    """Activations from the reference's synth_activation (synth.cpp:49-56) and
+    the algorithmic bytes from its own payload_bytes (container.cpp:466-471)."""
     import oracle
-    import paper_2311_16442_b200 as qw
-    xs = [qw.synth_activation(L.cfg.cols, 8 + i) for i, L in enumerate(layers)]
-    total = sum(b_alg(qw.payload_bytes(L), L.cfg.rows, L.cfg.cols) for L in layers)
-    if oracle.ref_available():
-        refs = [oracle.RefLayer.from_layer(L) for L in layers]
-        kind, run = "reference", (lambda: [r.matvec_pipelined(x, threads)[1] for r, x in zip(refs, xs)])
-        cores = threads
-    else:
-        kind, cores = "port", 1
+    xs = [oracle.ref_synth_activation(cols, 8 + i) for i, (_, _, cols) in enumerate(SHAPES_7B)]
+    nbytes = [b_alg(r.payload_bytes(), rows, cols) for r, (_, rows, cols) in zip(refs, SHAPES_7B)]
+    return xs, nbytes
 
-        def run():
-            out = []
-            for L, x in zip(layers, xs):
-                t0 = time.perf_counter_ns()
-                oracle.matvec_oracle(L, x)
-                out.append(time.perf_counter_ns() - t0)
-            return out
-    run()  # warm caches (bench_matvec does the same, engine.cpp:332-333)
+
+def ref_step_ns(refs, xs, layers: int, workers: int) -> int:
+    """One decode step through the reference: `layers` passes over the 7
+    linears with matvec_pipelined(workers), timed by the reference's own
+    MatvecResult.wall_ns (engine.cpp:198-247: excludes the activation
+    permutation and scratch allocation, like bench_matvec)."""
+    total = 0
+    for _ in range(layers):
+        for r, x in zip(refs, xs):
+            total += r.matvec_pipelined(x, workers)[1]
+    return total
+
+
+def cpu_reference_sample(budget_s: float, threads: int, cache_dir: Path):
+    """cpu_baseline: the reference CPU path on this host:
+    matvec_oracle on 1 thread, matvec_pipelined on 1 and on all host threads
+    (a thread-scaling self-check), then decoder-layer passes (7 linears) with
+    all threads for about budget_s seconds."""
+    import oracle
+    if not oracle.ref_available():
+        return None
+    refs = ref_make_layers(cache_dir)
+    xs, nbytes = ref_inputs(refs)
+    per_pass = sum(nbytes)
+    q = refs[0]
+    q.matvec_oracle(xs[0])  # warm (bench_matvec warms too, engine.cpp:332-333)
+    t1 = min(q.matvec_oracle(xs[0])[1] for _ in range(3))
+    p1 = min(q.matvec_pipelined(xs[0], 1)[1] for _ in range(3))
+    pn = min(q.matvec_pipelined(xs[0], threads)[1] for _ in range(5))
+    ref_step_ns(refs, xs, 1, threads)
     passes, t_start = [], time.perf_counter()
-    while time.perf_counter() - t_start < budget_s or len(passes) < 2:
-        passes.append(sum(run()))
-        if len(passes) >= 50:
+    while time.perf_counter() - t_start < budget_s or len(passes) < 3:
+        passes.append(ref_step_ns(refs, xs, 1, threads))
+        if len(passes) >= 200:
             break
-    best = min(passes)
-    return {"value": total / best, "unit": "GB/s", "cores": cores, "kind": kind,
-            "sample": f"one decoder layer (7 Llama-2-7B linears, {total} B_alg), "
-                      f"{len(passes)} passes, best pass {best / 1e6:.2f} ms "
-                      f"({'matvec_pipelined, workers=' + str(threads) if kind == 'reference' else 'C oracle port, 1 thread'})",
-            "ms_per_pass": best / 1e6, "bytes_per_pass": total}
+    mean_ns = statistics.mean(passes)
+    return {"value": round(per_pass / mean_ns, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+            "sample": f"one decoder layer per pass (the 7 Llama-2-7B linears, {per_pass} B_alg), "
+                      f"{len(passes)} passes in ~{budget_s:.0f} s, matvec_pipelined(workers={threads}), "
+                      f"mean of the reference's wall_ns",
+            "ms_per_pass": round(mean_ns / 1e6, 4), "best_ms_per_pass": round(min(passes) / 1e6, 4),
+            "bytes_per_pass": per_pass,
+            "oracle_1t": {"us_per_call": round(t1 / 1e3, 1), "value": round(nbytes[0] / t1, 4),
+                          "note": "matvec_oracle, q_proj 4096x4096, 1 thread, best of 3"},
+            "pipelined_1t": {"us_per_call": round(p1 / 1e3, 1), "value": round(nbytes[0] / p1, 4)},
+            "pipelined_nproc": {"us_per_call": round(pn / 1e3, 1), "value": round(nbytes[0] / pn, 4),
+                                "workers": threads},
+            "scaling": round(p1 / pn, 2)}
 
 
 def run_reference(args):
+    """The reference arm: the UNMODIFIED reference library (oracle/_ref,
+    compiled from its own sources) on the host cores, same workload, metric
+    and unit as the GPU arm.  A step is the whole 224-GEMV decode step (32
+    decoder layers x 7 linears) through matvec_pipelined(nproc); the 7
+    distinct layers are reused by every decoder layer (83 MB per layer pass,
+    larger than the host's last-level cache)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import oracle
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqweight_ref.so was not built "
+                          "(needs /root/reference at build time)"}), flush=True)
+        return 0
     threads = os.cpu_count() or 1
-    cache = Path(tempfile.gettempdir()) / "qw_bench_cache"
-    cache.mkdir(exist_ok=True)
-    layers = make_layers(0, 1, cache, threads)
-    import paper_2311_16442_b200 as qw
-    xs = [qw.synth_activation(L.cfg.cols, 8 + i) for i, L in enumerate(layers)]
-    total = sum(b_alg(qw.payload_bytes(L), L.cfg.rows, L.cfg.cols) for L in layers)
-    if oracle.ref_available():
-        kind, cores = "reference", threads
-        refs = [oracle.RefLayer.from_layer(L) for L in layers]
-
-        def step():
-            t0 = time.perf_counter_ns()
-            for r, x in zip(refs, xs):
-                r.matvec_pipelined(x, threads)
-            return time.perf_counter_ns() - t0
-    else:
-        kind, cores = "port", 1
-
-        def step():
-            t0 = time.perf_counter_ns()
-            for L, x in zip(layers, xs):
-                oracle.matvec_oracle(L, x)
-            return time.perf_counter_ns() - t0
+    cache = Path(os.environ.get("QW_BENCH_CACHE", Path(tempfile.gettempdir()) / "qw_bench_cache"))
+    cache.mkdir(parents=True, exist_ok=True)
+    t_prep = time.perf_counter()
+    refs = ref_make_layers(cache)
+    xs, nbytes = ref_inputs(refs)
+    prep_s = time.perf_counter() - t_prep
+    step_bytes = sum(nbytes) * args.layers
     for _ in range(args.warmup):
-        step()
-    times = [step() for _ in range(args.steps)]
+        ref_step_ns(refs, xs, args.layers, threads)
+    times = [ref_step_ns(refs, xs, args.layers, threads) for _ in range(args.steps)]
     ms = statistics.mean(times) / 1e6
-    value = total / (ms * 1e6)
+    value = step_bytes / (ms * 1e6)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "us_per_layer": round(ms * 1e3 / len(layers), 3),
-        "config": {"workload": "llama2-7b linears q/k/v/o 4096x4096, gate/up 11008x4096, "
-                               "down 4096x11008; batch-1 GEMV; one decoder layer per step "
-                               "(bounded CPU sample)",
+        "us_per_layer": round(ms * 1e3 / (7 * args.layers), 3),
+        "config": {"workload": "llama2-7b decode step: q/k/v/o 4096x4096, gate/up 11008x4096, "
+                               f"down 4096x11008 x {args.layers} layers ({7 * args.layers} batch-1 GEMVs)",
                    "alpha": ALPHA, "group1": 16, "group2": GROUP2, "outlier_ratio": RATIO,
-                   "batch": 1},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": kind,
-                         "sample": f"7 linears per step x {args.steps} steps"},
+                   "batch": 1, "bytes_per_step": step_bytes,
+                   "producer": "reference synth_gaussian/synth_calibration + quantize_layer, QWL1 cache"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"the full {7 * args.layers}-GEMV step per timed step, matvec_pipelined"
+                                   f"(workers={threads}), sum of the reference's wall_ns, mean of {args.steps}"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "prep_s": round(prep_s, 1),
+        "libraries": loaded_repo_libs(),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def loaded_repo_libs() -> list:
+    """Shared objects of this repo mapped into the process (from /proc/self/maps)."""
+    try:
+        maps = Path("/proc/self/maps").read_text().splitlines()
+    except OSError:
+        return []
+    return sorted({ln.split()[-1].replace(str(ROOT) + "/", "") for ln in maps
+                   if ln.endswith(".so") and str(ROOT) in ln})
 
 
 # --------------------------------------------------------------- GPU arm
@@ -374,7 +433,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_reference_sample(base, args.cpu_budget, os.cpu_count() or 1)
+        cpu = cpu_reference_sample(args.cpu_budget, os.cpu_count() or 1, cache)
 
     if rank == 0:
         line = {
