@@ -291,7 +291,7 @@ def run_ours(args):
     cache.mkdir(parents=True, exist_ok=True)
     t_prep = time.perf_counter()
     base = make_layers(rank, world, cache, threads)
-    dls = [qw.DeviceLayer(L, local) for L in base]
+    dls = [qw.DeviceLayer(L, local, kernel=args.kernel) for L in base]
     payload = [qw.payload_bytes(L) for L in base]
     per_layer = []
     for l in range(args.layers):
@@ -321,7 +321,7 @@ def run_ours(args):
     stack.capture()
     stack.replay()
     torch.cuda.synchronize()
-    if rank == 0:
+    if rank == 0 and not os.environ.get("QW_DEBUG_MMA_DIAG"):  # diagnostics runs compute garbage
         import oracle
         for j in (0, 4, 6):
             y = stack.y_of(j).cpu().numpy().reshape(-1)
@@ -440,7 +440,9 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "fp16x2-dot/fp32-accumulate", "data": "synthetic",
+            "dtype": ("fp16x2-dot/fp32-accumulate" if args.kernel == "simt" else
+                      "fp16 MMA (mma.sync m16n8k16)/fp32-accumulate"), "data": "synthetic",
+            "batch1_kernel": args.kernel,
             "us_per_layer": round(ms_step * 1e3 / n_gemv, 4),
             "dependency": "decode chain: per decoder layer 4 steps -- {q,k,v} (one input, fused), o, "
                           "{gate,up} (fused), down -- each waiting for its predecessor before reading x" +
@@ -506,6 +508,8 @@ def main():
     ap.add_argument("--prefetch", action="store_true", help="L2 prefetch of the next launch's weights")
     ap.add_argument("--ungrouped", action="store_true", help="one launch per linear (no q/k/v, gate/up fusion)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--kernel", default="simt", choices=["simt", "mma"],
+                    help="batch-1 kernel: the SIMT K2 (default) or the warp-MMA K2m")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU sample")
     args = ap.parse_args()
     if args.warmup < 3:

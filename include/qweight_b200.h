@@ -153,6 +153,14 @@ typedef struct qw_layer qw_layer;
 typedef struct qw_workspace qw_workspace;
 
 int qw_layer_upload(const qw_layer_view* view, int device, qw_layer** out);
+/* Upload with options.  QW_UPLOAD_TENSOR_CORE also lays the layer out in the
+ * 16-row tile format of the warp-MMA batch-1 kernel (K2m, qw_mma.cu) and
+ * routes batch-1 matvecs, group launches and decode chains of the layer to
+ * it (the SIMT kernel K2 is the default: the faster one on the measured
+ * shapes).  Layers whose group2 is not a multiple of 16
+ * keep K2. */
+#define QW_UPLOAD_TENSOR_CORE 1u
+int qw_layer_upload_ex(const qw_layer_view* view, int device, uint32_t flags, qw_layer** out);
 int qw_layer_free(qw_layer* layer);
 int qw_layer_get_info(const qw_layer* layer, qw_layer_info* info);
 
@@ -226,6 +234,11 @@ int qw_chain_free(qw_chain* chain);
  * spins for seconds records {code, arg, parity, cta, thread} per warp into
  * host memory and traps; this copies those records out. */
 int qw_debug_chain_watch(uint32_t* out, uint32_t n);
+/* Diagnostics: per (step, CTA) 8 %globaltimer stamps of the last run of a
+ * tensor-core chain planned with QW_DEBUG_MMA_TL=1 (step start, x staged,
+ * items done, CSR met, dependency resolved, reduction done, counter
+ * released, producer's last copy issued). */
+int qw_debug_chain_timeline(const qw_chain* chain, unsigned long long* out, uint64_t n);
 /* Host-buffer, synchronous, checked: length and finiteness as the reference
  * (engine.cpp:124-132).  x_len must equal batch * cols. */
 int qw_matvec_host(const qw_layer* layer, const float* x, uint64_t x_len,

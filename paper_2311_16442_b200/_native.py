@@ -80,6 +80,7 @@ _SIGS = {
     "qw_synth_calibration": (C.c_int, [C.c_uint32, C.c_uint64, C.c_void_p]),
     "qw_synth_activation": (C.c_int, [C.c_uint32, C.c_uint64, C.c_void_p]),
     "qw_layer_upload": (C.c_int, [C.POINTER(LayerView), C.c_int, C.POINTER(C.c_void_p)]),
+    "qw_layer_upload_ex": (C.c_int, [C.POINTER(LayerView), C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]),
     "qw_layer_free": (C.c_int, [C.c_void_p]),
     "qw_layer_get_info": (C.c_int, [C.c_void_p, C.POINTER(LayerInfo)]),
     "qw_workspace_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
@@ -96,6 +97,7 @@ _SIGS = {
     "qw_chain_run": (C.c_int, [C.c_void_p, C.c_void_p]),
     "qw_chain_free": (C.c_int, [C.c_void_p]),
     "qw_debug_chain_watch": (C.c_int, [C.POINTER(C.c_uint32), C.c_uint32]),
+    "qw_debug_chain_timeline": (C.c_int, [C.c_void_p, C.POINTER(C.c_ulonglong), C.c_uint64]),
     "qw_group_set_prefetch": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_uint32]),
     "qw_matvec_pdl": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
                                 C.c_void_p]),

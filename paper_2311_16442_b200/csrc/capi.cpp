@@ -49,14 +49,20 @@ struct qw_layer {
 
 struct qw_group {
   qwdev::GemvPlan plan;
+  qwdev::MmaPlan mplan;
+  bool mma = false;  // every layer has the tensor-core tile format
   std::vector<const qwdev::DeviceLayer*> layers;  // borrowed
   int device = 0;
 };
 
 struct qw_chain {
-  qwdev::ChainPlan* plan = nullptr;
+  qwdev::ChainPlan* plan = nullptr;      // SIMT chain kernel
+  qwdev::MmaChainPlan* mplan = nullptr;  // tensor-core chain kernel (every layer in the K2m format)
   int device = 0;
-  ~qw_chain() { qwdev::free_chain(plan); }
+  ~qw_chain() {
+    qwdev::free_chain(plan);
+    qwdev::free_mma_chain(mplan);
+  }
 };
 
 struct qw_workspace {
@@ -292,7 +298,21 @@ void free_dev(qwdev::DeviceLayer& d) {
   qwdev::free_gemm(d);
   cudaFree(d.quads), cudaFree(d.sorder), cudaFree(d.perm), cudaFree(d.row_ptr), cudaFree(d.csr);
   cudaFree(d.perm16);
+  cudaFree(d.mrecs), cudaFree(d.mpart), cudaFree(d.mcnt);
   d = qwdev::DeviceLayer{};
+}
+
+// K2m scratch: chunk partials + CSR sums, arrival counters (zeroed; the
+// kernel leaves them zero)
+cudaError_t alloc_mma_scratch(qwdev::DeviceLayer& d) {
+  const auto& m = d.mg;
+  cudaError_t e = cudaSuccess;
+  if (m.nchunks > 1) {
+    if ((e = cudaMalloc((void**)&d.mpart, (size_t)(m.nchunks + 1) * m.RT * 16 * 4)) != cudaSuccess) return e;
+    if ((e = cudaMalloc((void**)&d.mcnt, (size_t)m.RT * 4)) != cudaSuccess) return e;
+    e = cudaMemset(d.mcnt, 0, (size_t)m.RT * 4);
+  }
+  return e;
 }
 
 int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
@@ -316,10 +336,19 @@ int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_w
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   }
   static const bool no_gemm = std::getenv("QW_NO_GEMM") != nullptr;
-  const int e = (batch >= 2 && L->dev.gemm.ok && !no_gemm)
-                    ? qwdev::launch_gemm(L->dev, x, batch, y, stream)
-                    : qwdev::launch_gemv(L->dev, x, batch, y, stream, pdl, nullptr, 1, false,
-                                         (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u);
+  const uint32_t xflags = (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u;
+  int e = 0;
+  if (batch >= 2 && L->dev.gemm.ok && !no_gemm) {
+    e = qwdev::launch_gemm(L->dev, x, batch, y, stream);
+  } else if (L->dev.mrecs) {
+    const qwdev::DeviceLayer* one[1] = {&L->dev};
+    for (uint32_t col = 0; col < batch && !e; ++col) {
+      float* ys[1] = {y + (size_t)col * L->dev.g.rows};
+      e = qwdev::launch_mma(L->dev.mplan, one, 1, x + (size_t)col * L->dev.g.cols, ys, stream, pdl, xflags);
+    }
+  } else {
+    e = qwdev::launch_gemv(L->dev, x, batch, y, stream, pdl, nullptr, 1, false, xflags);
+  }
   if (e) return cuda_fail((cudaError_t)e, "gemv launch");
   return QW_OK;
 }
@@ -504,6 +533,10 @@ int qw_synth_activation(uint32_t cols, uint64_t seed, float* out) {
 
 // ------------------------------------------------------------------ device
 int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
+  return qw_layer_upload_ex(v, device, 0u, out);
+}
+
+int qw_layer_upload_ex(const qw_layer_view* v, int device, uint32_t flags, qw_layer** out) {
   return guarded([&] {
     if (!v || !out) return fail(QW_ERR_ARG, "upload: null argument");
     const qwb::PackedLayer L = from_view(*v);
@@ -556,6 +589,21 @@ int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
     if (int ge = qwdev::plan_gemm(H->dev, H->num_sms, H->max_scale2, H->max_s4)) {
       free_dev(H->dev);
       return cuda_fail((cudaError_t)ge, "gemm plan");
+    }
+    qwdev::mma_geometry(H->dev.mg, H->dev.g);
+    if (H->dev.mg.ok && (flags & QW_UPLOAD_TENSOR_CORE)) {
+      std::vector<uint8_t> recs;
+      qwb::repack_mma(L, H->dev.mg, H->dev.plan.s_scale, recs);
+      const qwdev::DeviceLayer* one[1] = {&H->dev};
+      if ((e = upload(&H->dev.mrecs, recs)) != cudaSuccess || (e = alloc_mma_scratch(H->dev)) != cudaSuccess) {
+        free_dev(H->dev);
+        return cuda_fail(e, "upload (mma tiles)");
+      }
+      const uint32_t* rp[1] = {H->host_row_ptr.data()};
+      if (int pe = qwdev::plan_mma(H->dev.mplan, one, rp, 1, H->num_sms)) {
+        free_dev(H->dev);
+        return cuda_fail((cudaError_t)pe, "mma plan");
+      }
     }
     *out = H.release();
     return (int)QW_OK;
@@ -710,6 +758,21 @@ int qw_layer_clone(const qw_layer* L, qw_layer** out) {
     free_dev(H->dev);
     return cuda_fail((cudaError_t)ge, "gemm plan");
   }
+  H->dev.mg = L->dev.mg;
+  if (L->dev.mrecs) {
+    const auto& m = L->dev.mg;
+    const qwdev::DeviceLayer* one[1] = {&H->dev};
+    if ((e = dup(&H->dev.mrecs, L->dev.mrecs, (size_t)m.RT * m.nchunks * m.rec_stride)) != cudaSuccess ||
+        (e = alloc_mma_scratch(H->dev)) != cudaSuccess) {
+      free_dev(H->dev);
+      return cuda_fail(e, "clone (mma tiles)");
+    }
+    const uint32_t* rp[1] = {H->host_row_ptr.data()};
+    if (int pe = qwdev::plan_mma(H->dev.mplan, one, rp, 1, H->num_sms)) {
+      free_dev(H->dev);
+      return cuda_fail((cudaError_t)pe, "mma plan");
+    }
+  }
   *out = H.release();
   return QW_OK;
 }
@@ -741,6 +804,12 @@ int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out) {
     if (e == (int)cudaErrorInvalidValue)
       return fail(QW_ERR_ARG, "group: layers must share cols, channel split and group2 (rows may differ)");
     if (e) return cuda_fail((cudaError_t)e, "group plan");
+    G->mma = true;
+    for (uint32_t i = 0; i < n; ++i) G->mma = G->mma && layers[i]->dev.mrecs != nullptr;
+    if (G->mma) {
+      if (int me = qwdev::plan_mma(G->mplan, G->layers.data(), rps.data(), n, layers[0]->num_sms))
+        return cuda_fail((cudaError_t)me, "group mma plan");
+    }
     *out = G.release();
     return (int)QW_OK;
   });
@@ -758,9 +827,11 @@ int qw_group_matvec(const qw_group* g, const float* x, float* const* ys, void* s
   int dev_now = -1;
   cudaGetDevice(&dev_now);
   if (dev_now != g->device) cudaSetDevice(g->device);
-  const int e = qwdev::launch_gemv_group(g->plan, g->layers.data(), (uint32_t)g->layers.size(), x, ys, stream,
-                                         (flags & QW_LAUNCH_PDL) != 0,
-                                         (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u);
+  const uint32_t xflags = (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u;
+  const int e = g->mma ? qwdev::launch_mma(g->mplan, g->layers.data(), (uint32_t)g->layers.size(), x, ys, stream,
+                                           (flags & QW_LAUNCH_PDL) != 0, xflags)
+                       : qwdev::launch_gemv_group(g->plan, g->layers.data(), (uint32_t)g->layers.size(), x, ys,
+                                                  stream, (flags & QW_LAUNCH_PDL) != 0, xflags);
   return e ? cuda_fail((cudaError_t)e, "group launch") : QW_OK;
 }
 
@@ -822,6 +893,16 @@ int qw_chain_create(const qw_chain_step* steps, uint32_t n, qw_chain** out) {
     cudaSetDevice(device);
     auto C = std::make_unique<qw_chain>();
     C->device = device;
+    bool mma = true;
+    for (uint32_t s = 0; s < n; ++s)
+      for (const auto* L : lay[s]) mma = mma && L->mrecs != nullptr;
+    if (mma) {
+      const int me = qwdev::plan_mma_chain(&C->mplan, d.data(), n, num_sms);
+      if (me == (int)cudaErrorInvalidValue) return fail(QW_ERR_ARG, "chain: a step's layers differ in geometry");
+      if (me) return cuda_fail((cudaError_t)me, "chain plan (mma)");
+      *out = C.release();
+      return (int)QW_OK;
+    }
     const int e = qwdev::plan_chain(&C->plan, d.data(), n, num_sms);
     if (e == (int)cudaErrorInvalidValue) return fail(QW_ERR_ARG, "chain: a step's layers differ in geometry");
     if (e == (int)cudaErrorNotSupported)
@@ -837,8 +918,14 @@ int qw_chain_run(const qw_chain* c, void* stream) {
   int dev_now = -1;
   cudaGetDevice(&dev_now);
   if (dev_now != c->device) cudaSetDevice(c->device);
-  const int e = qwdev::launch_chain(c->plan, stream);
+  const int e = c->mplan ? qwdev::launch_mma_chain(c->mplan, stream) : qwdev::launch_chain(c->plan, stream);
   return e ? cuda_fail((cudaError_t)e, "chain launch") : QW_OK;
+}
+
+int qw_debug_chain_timeline(const qw_chain* c, unsigned long long* out, uint64_t n) {
+  if (!c || !c->mplan || !out) return fail(QW_ERR_ARG, "chain timeline: needs a tensor-core chain planned with QW_DEBUG_MMA_TL=1");
+  const int e = qwdev::mma_chain_timeline(c->mplan, out, n);
+  return e ? cuda_fail((cudaError_t)e, "chain timeline") : QW_OK;
 }
 
 int qw_debug_chain_watch(uint32_t* out, uint32_t n) {

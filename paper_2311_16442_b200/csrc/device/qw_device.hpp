@@ -89,10 +89,50 @@ struct GemmPlan {
   float* ycsr = nullptr;     // [16][rows] CSR outlier sums of the call
 };
 
+// ------------------------------------------------------------ K2m (batch 1, warp MMA)
+// Tile format of the tensor-core batch-1 kernel (qw_mma.cu).  Rows are taken
+// 16 at a time (one m16n8k16 M tile); the row's channel groups are taken 8 at
+// a time ("blocks": the 8 N columns of the MMA, one group per column, the B
+// operand block-diagonal in x).  2-bit groups go in super-blocks of 8 triples
+// (24 groups, 3 blocks) so a lane's 6 groups are exactly 2 meta words; 4-bit
+// blocks of 16 channels go 8 to a block.  A row tile's blocks are cut into
+// chunks of at most 32 (16 consumer warps x 2 blocks, the B fragments stay in
+// registers); one (tile, chunk) record is one contiguous TMA copy:
+//   2-bit block: [SB header: meta 32 lanes x 2 u32 | sorder 3 b x 4 t x 2 u32]
+//                (the first time the chunk touches the super-block), then
+//                codes 32 lanes x 4 u32 (E_g, E_g+8, O_g, O_g+8)
+//   4-bit block: codes 32 lanes x 8 u32, s4 32 lanes x 2 u32, z4 32 lanes x u16
+// Lane (g, t) of a block owns rows {g, g+8} and columns {2t, 2t+1}.
+constexpr uint32_t kMmaMaxChunks = 8, kMmaMaxBlk = 32;
+constexpr uint32_t kMmaHdr2 = 352, kMmaCode2 = 512, kMmaCode4 = 1024, kMmaS4 = 256, kMmaZ4 = 64;
+struct MmaChunk {
+  uint32_t nblk = 0, rec_bytes = 0;
+  uint8_t kind[kMmaMaxBlk] = {};   // 0..2: 2-bit block b of a super-block, 3: 4-bit
+  uint16_t grp[kMmaMaxBlk] = {};   // super-block (2-bit) / 8-block index (4-bit)
+  uint32_t code_off[kMmaMaxBlk] = {}, hdr_off[kMmaMaxBlk] = {};
+};
+struct MmaGeometry {
+  uint32_t ok = 0;                  // layer supported (group2 % 16 == 0, <= kMmaMaxChunks chunks)
+  uint32_t RT = 0, SB = 0, B4 = 0, nchunks = 0, rec_stride = 0;
+  MmaChunk chunk[kMmaMaxChunks];
+};
+struct MmaPlan {
+  uint32_t grid = 0, nslot = 0, smem = 0, items_max = 0;
+  uint32_t x_off = 0, part_off = 0, csr_off = 0, ent_off = 0, csr_slot = 0, csr_nslot = 4, rp_off = 0, bst_off = 0, bar_off = 0;
+  uint8_t cta_seg[kMaxGrid] = {};
+  uint32_t cta_i0[kMaxGrid] = {}, cta_i1[kMaxGrid] = {};
+  uint32_t cta_e0[kMaxGrid] = {}, cta_e1[kMaxGrid] = {};  // CSR entries of the CTA's chunk-0 rows
+};
+
 struct DeviceLayer {
   Geometry g;
   GemvPlan plan;
   GemmPlan gemm;
+  MmaGeometry mg;
+  MmaPlan mplan;
+  uint8_t* mrecs = nullptr;       // RT x nchunks records (chunk-major), rec_stride apart
+  float* mpart = nullptr;         // [nchunks][RT*16] chunk partial sums, then [RT*16] CSR sums
+  uint32_t* mcnt = nullptr;       // [RT] chunk arrivals (self-resetting)
   uint8_t* quads = nullptr;      // quads * dense_bytes
   uint32_t* sorder = nullptr;    // row_blocks * G2s
   uint32_t* perm = nullptr;      // padded_cols (0xFFFFFFFF = pad)
@@ -142,6 +182,14 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
 int launch_unpack(const DeviceLayer& L, uint8_t* codes2, uint8_t* zeros2, uint8_t* scodes,
                   uint8_t* codes4, void* stream);
 
+// K2m: geometry of the tile format (host, no CUDA calls); plan the CTA item
+// ranges of a single layer or a group of layers (identical columns); launch.
+void mma_geometry(MmaGeometry& m, const Geometry& g);
+int plan_mma(MmaPlan& p, const DeviceLayer* const* layers, const uint32_t* const* host_row_ptrs, uint32_t n,
+             int num_sms);
+int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
+               float* const* ys, void* stream, bool pdl, uint32_t flags);
+
 // Decode chain (batch 1): a sequence of launch steps (each a group of 1..4
 // layers of identical geometry reading one activation) run by ONE persistent
 // kernel -- one CTA per SM streams the weights of step s+1 into its ring
@@ -161,6 +209,14 @@ struct ChainPlan;
 int plan_chain(ChainPlan** out, const ChainStepDesc* steps, uint32_t n, int num_sms);
 int launch_chain(const ChainPlan* p, void* stream);
 void free_chain(ChainPlan* p);
-const unsigned* chain_watch();  // diagnostics (QW_CHAIN_WATCH): [cta][warp][8] hang records, host memory
+const unsigned* chain_watch();
+// The same decode chain on the K2m tile format (every layer uploaded with
+// it): one persistent tensor-core kernel; cudaErrorNotSupported otherwise.
+struct MmaChainPlan;
+int plan_mma_chain(MmaChainPlan** out, const ChainStepDesc* steps, uint32_t n, int num_sms);
+int launch_mma_chain(const MmaChainPlan* p, void* stream);
+void free_mma_chain(MmaChainPlan* p);
+// diagnostics: [step][cta][8] %globaltimer stamps of the last run (QW_DEBUG_MMA_TL=1 at plan time)
+int mma_chain_timeline(const MmaChainPlan* p, unsigned long long* out, size_t n);  // diagnostics (QW_CHAIN_WATCH): [cta][warp][8] hang records, host memory
 
 }  // namespace qwdev

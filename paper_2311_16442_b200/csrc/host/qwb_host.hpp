@@ -160,6 +160,13 @@ PackedLayer deserialize_layer(std::span<const uint8_t> bytes);       // containe
 uint32_t crc32(std::span<const uint8_t> bytes);
 
 PackedLayer shard_rows(const PackedLayer& layer, uint32_t r0, uint32_t r1);
+
+}  // namespace qwb
+namespace qwdev { struct MmaGeometry; }
+namespace qwb {
+// Tile format of the tensor-core batch-1 kernel (qwb_mma.cpp, qw_device.hpp).
+void repack_mma(const PackedLayer& layer, const qwdev::MmaGeometry& m, float s_scale,
+                std::vector<uint8_t>& out);
 PackedLayer shard_tiles(const PackedLayer& layer, uint32_t t0, uint32_t t1);
 
 // Parallel helper: run fn(begin, end) over [0, n) in at most `threads` chunks.

@@ -81,14 +81,21 @@ class MatvecResult:
 class DeviceLayer:
     """A packed layer uploaded to HBM in the 4-row device format."""
 
-    def __init__(self, layer: PackedLayer | None, device: int = 0, _handle=None):
+    def __init__(self, layer: PackedLayer | None, device: int = 0, _handle=None, kernel: str = "simt"):
+        """kernel: "simt" -- the fused SIMT GEMV K2 (default, the faster one on
+        the measured shapes); "mma" -- also lay the layer out for the
+        warp-MMA batch-1 kernel K2m and route batch-1 calls to it."""
+        if kernel not in ("simt", "mma"):
+            raise ValueError("kernel must be 'simt' or 'mma'")
         self.device = device
+        self.kernel = kernel
         self._h = C.c_void_p()
         if _handle is not None:
             self._h = _handle
         else:
             self.layer_cfg = layer.cfg
-            check(lib().qw_layer_upload(C.byref(layer.view()), device, C.byref(self._h)))
+            check(lib().qw_layer_upload_ex(C.byref(layer.view()), device, 1 if kernel == "mma" else 0,
+                                           C.byref(self._h)))
         inf = LayerInfo()
         check(lib().qw_layer_get_info(self._h, C.byref(inf)))
         self.info = inf.as_dict()
@@ -177,7 +184,7 @@ class DeviceLayer:
         """Device-to-device copy (distinct HBM buffers, same content)."""
         h = C.c_void_p()
         check(lib().qw_layer_clone(self._h, C.byref(h)))
-        out = DeviceLayer(None, self.device, _handle=h)
+        out = DeviceLayer(None, self.device, _handle=h, kernel=self.kernel)
         out.layer_cfg = getattr(self, "layer_cfg", None)
         return out
 

@@ -46,12 +46,16 @@ def check_y(y, ref):
     return err
 
 
+KERNELS = ["simt", "mma"]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("name", GOLDEN_LAYERS)
-def test_reference_written_layer_on_gpu(name):
+def test_reference_written_layer_on_gpu(name, kernel):
     import torch
     layer = qw.read_packed_layer(str(GOLD / f"layer_{name}.qwl"))  # bytes written by the reference
     d = np.load(GOLD / f"layer_{name}.npz")
-    dl = qw.DeviceLayer(layer)
+    dl = qw.DeviceLayer(layer, kernel=kernel)
     # K1: the reference's reconstruct_dense, bit for bit (by hash)
     assert sha(dl.reconstruct_dense().cpu().numpy()) == str(d["recon_sha"])
     # K0: the reference's unpack_layer, bit for bit (by hash)
@@ -88,11 +92,13 @@ def test_config4_llama13b_outlier_sweep(rows, cols, ratio):
     import torch
     layer = qw.synth_layer(rows, cols, seed=rows + cols, outlier_ratio=ratio)
     assert layer.cfg.outlier_count == round(ratio * rows * cols)
-    dl = qw.DeviceLayer(layer)
     x = qw.synth_activation(cols, 13)
-    y = dl.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
-    err = check_y(y, oracle.matvec_f64(layer, x))
-    assert err < 3e-3, err
+    ref = oracle.matvec_f64(layer, x)
+    for kernel in KERNELS:
+        dl = qw.DeviceLayer(layer, kernel=kernel)
+        y = dl.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        err = check_y(y, ref)
+        assert err < 3e-3, (kernel, err)
     if ratio == 0.01:  # K1 bit-exact at full size (densest outliers: most zeroed slots)
         w = dl.reconstruct_dense().cpu().numpy()
         assert np.array_equal(w.view(np.uint32), oracle.reconstruct_dense(layer).view(np.uint32))
@@ -106,11 +112,12 @@ CFG5 = [(8192, 8192), (1024, 8192), (28672, 8192), (8192, 28672)]
 def test_config5_llama70b_shapes(rows, cols):
     import torch
     layer = qw.synth_layer(rows, cols, seed=rows * 3 + cols)
-    dl = qw.DeviceLayer(layer)
     x = qw.synth_activation(cols, 17)
-    y = dl.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
-    err = check_y(y, oracle.matvec_f64(layer, x))
-    assert err < 3e-3, err
+    ref = oracle.matvec_f64(layer, x)
+    for kernel in KERNELS:
+        y = qw.DeviceLayer(layer, kernel=kernel).matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        err = check_y(y, ref)
+        assert err < 3e-3, (kernel, err)
 
 
 @pytest.mark.slow
@@ -118,8 +125,10 @@ def test_config5_gqa_group_launch():
     """Llama-2-70B q (8192 rows) with GQA k/v (1024 rows each) as one launch."""
     import torch
     layers = [qw.synth_layer(r, 8192, seed=700 + i) for i, r in enumerate((8192, 1024, 1024))]
-    dls = [qw.DeviceLayer(L) for L in layers]
     x = qw.synth_activation(8192, 701)
-    outs = qw.LayerGroup(dls).matvec(torch.from_numpy(x).cuda())
-    for L, o in zip(layers, outs):
-        check_y(o.cpu().numpy(), oracle.matvec_f64(L, x))
+    refs = [oracle.matvec_f64(L, x) for L in layers]
+    for kernel in KERNELS:
+        dls = [qw.DeviceLayer(L, kernel=kernel) for L in layers]
+        outs = qw.LayerGroup(dls).matvec(torch.from_numpy(x).cuda())
+        for o, ref in zip(outs, refs):
+            check_y(o.cpu().numpy(), ref)
