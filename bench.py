@@ -440,9 +440,9 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": ("fp16x2-dot/fp32-accumulate" if args.kernel == "simt" else
+            "dtype": ("fp16x2-dot/fp32-accumulate" if not dls[0].uses_tensor_core else
                       "fp16 MMA (mma.sync m16n8k16)/fp32-accumulate"), "data": "synthetic",
-            "batch1_kernel": args.kernel,
+            "batch1_kernel": "K2m (warp MMA)" if dls[0].uses_tensor_core else "K2 (SIMT)",
             "us_per_layer": round(ms_step * 1e3 / n_gemv, 4),
             "dependency": "decode chain: per decoder layer 4 steps -- {q,k,v} (one input, fused), o, "
                           "{gate,up} (fused), down -- each waiting for its predecessor before reading x" +
@@ -508,8 +508,8 @@ def main():
     ap.add_argument("--prefetch", action="store_true", help="L2 prefetch of the next launch's weights")
     ap.add_argument("--ungrouped", action="store_true", help="one launch per linear (no q/k/v, gate/up fusion)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--kernel", default="simt", choices=["simt", "mma"],
-                    help="batch-1 kernel: the SIMT K2 (default) or the warp-MMA K2m")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "mma"],
+                    help="batch-1 kernel: auto (K2 here: every 7B shape fits its CSR stage), simt (K2), mma (K2m)")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU sample")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -153,16 +153,22 @@ typedef struct qw_layer qw_layer;
 typedef struct qw_workspace qw_workspace;
 
 int qw_layer_upload(const qw_layer_view* view, int device, qw_layer** out);
-/* Upload with options.  QW_UPLOAD_TENSOR_CORE also lays the layer out in the
- * 16-row tile format of the warp-MMA batch-1 kernel (K2m, qw_mma.cu) and
- * routes batch-1 matvecs, group launches and decode chains of the layer to
- * it (the SIMT kernel K2 is the default: the faster one on the measured
- * shapes).  Layers whose group2 is not a multiple of 16
- * keep K2. */
+/* Upload with options: which batch-1 kernel serves the layer.
+ *   0 (auto, what qw_layer_upload does): the SIMT kernel K2, except where
+ *     the measured shape sweep has the warp-MMA kernel
+ *     K2m ahead -- layers whose outliers do not fit K2's shared-memory CSR
+ *     stage (K2 then falls back to a global-memory CSR loop) and layers
+ *     wider than K2's two-groups-per-lane limit (70B down_proj);
+ *   QW_UPLOAD_TENSOR_CORE: always K2m (16-row tile format, qw_mma.cu);
+ *   QW_UPLOAD_SIMT: always K2.
+ * Layers whose group2 is not a multiple of 16 always keep K2. */
 #define QW_UPLOAD_TENSOR_CORE 1u
+#define QW_UPLOAD_SIMT 2u
 int qw_layer_upload_ex(const qw_layer_view* view, int device, uint32_t flags, qw_layer** out);
 int qw_layer_free(qw_layer* layer);
 int qw_layer_get_info(const qw_layer* layer, qw_layer_info* info);
+/* 1 when batch-1 calls of the layer run K2m (the warp-MMA kernel), 0 for K2. */
+int qw_layer_uses_tensor_core(const qw_layer* layer);
 
 /* Scratch for one stream (up to max_batch columns of up to max_cols
  * channels).  The fused batch-1 kernel needs none; kept for the batched

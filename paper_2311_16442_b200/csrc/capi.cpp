@@ -591,7 +591,12 @@ int qw_layer_upload_ex(const qw_layer_view* v, int device, uint32_t flags, qw_la
       return cuda_fail((cudaError_t)ge, "gemm plan");
     }
     qwdev::mma_geometry(H->dev.mg, H->dev.g);
-    if (H->dev.mg.ok && (flags & QW_UPLOAD_TENSOR_CORE)) {
+    // batch-1 kernel policy (header): auto picks K2m where K2's plan falls
+    // back to the global-memory CSR loop or exceeds two groups per lane
+    const auto& gp = H->dev.plan;
+    const bool k2_slow = (L.csr.nnz() > 0 && !gp.csr_stage) || (gp.kmax > 2 && !gp.wide) || !gp.xsm;
+    const bool want_mma = (flags & QW_UPLOAD_TENSOR_CORE) || (!(flags & QW_UPLOAD_SIMT) && k2_slow);
+    if (H->dev.mg.ok && want_mma) {
       std::vector<uint8_t> recs;
       qwb::repack_mma(L, H->dev.mg, H->dev.plan.s_scale, recs);
       const qwdev::DeviceLayer* one[1] = {&H->dev};
@@ -617,6 +622,8 @@ int qw_layer_free(qw_layer* L) {
   delete L;
   return QW_OK;
 }
+
+int qw_layer_uses_tensor_core(const qw_layer* L) { return L && L->dev.mrecs ? 1 : 0; }
 
 int qw_layer_get_info(const qw_layer* L, qw_layer_info* info) {
   if (!L || !info) return fail(QW_ERR_ARG, "info: null argument");

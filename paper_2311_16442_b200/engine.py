@@ -81,12 +81,12 @@ class MatvecResult:
 class DeviceLayer:
     """A packed layer uploaded to HBM in the 4-row device format."""
 
-    def __init__(self, layer: PackedLayer | None, device: int = 0, _handle=None, kernel: str = "simt"):
-        """kernel: "simt" -- the fused SIMT GEMV K2 (default, the faster one on
-        the measured shapes); "mma" -- also lay the layer out for the
-        warp-MMA batch-1 kernel K2m and route batch-1 calls to it."""
-        if kernel not in ("simt", "mma"):
-            raise ValueError("kernel must be 'simt' or 'mma'")
+    def __init__(self, layer: PackedLayer | None, device: int = 0, _handle=None, kernel: str = "auto"):
+        """kernel (batch-1 path): "auto" -- the SIMT GEMV K2 except where the
+        warp-MMA kernel K2m measured faster (dense outliers that overflow K2's
+        CSR stage, very wide layers; qweight_b200.h); "simt" / "mma" force one."""
+        if kernel not in ("auto", "simt", "mma"):
+            raise ValueError("kernel must be 'auto', 'simt' or 'mma'")
         self.device = device
         self.kernel = kernel
         self._h = C.c_void_p()
@@ -94,11 +94,16 @@ class DeviceLayer:
             self._h = _handle
         else:
             self.layer_cfg = layer.cfg
-            check(lib().qw_layer_upload_ex(C.byref(layer.view()), device, 1 if kernel == "mma" else 0,
-                                           C.byref(self._h)))
+            flags = {"auto": 0, "mma": 1, "simt": 2}[kernel]
+            check(lib().qw_layer_upload_ex(C.byref(layer.view()), device, flags, C.byref(self._h)))
         inf = LayerInfo()
         check(lib().qw_layer_get_info(self._h, C.byref(inf)))
         self.info = inf.as_dict()
+
+    @property
+    def uses_tensor_core(self) -> bool:
+        """True when batch-1 calls run the warp-MMA kernel K2m."""
+        return bool(lib().qw_layer_uses_tensor_core(self._h))
 
     @property
     def rows(self): return self.info["rows"]

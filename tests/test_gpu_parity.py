@@ -411,3 +411,20 @@ def test_linear_stack_run_end_to_end():
             y = out[off:off + L.cfg.rows]
             off += L.cfg.rows
             assert np.array_equal(y, d.matvec(torch.from_numpy(x).cuda()).cpu().numpy())
+
+
+def test_auto_kernel_policy():
+    """kernel="auto": K2 (SIMT) where it measured faster, K2m (warp MMA) for
+    outliers that overflow K2's CSR stage and for layers wider than 16384."""
+    dense = qw.synth_layer(5120, 13824, seed=3, outlier_ratio=0.01)  # Llama-2-13B down_proj, 1 %
+    wide = qw.synth_layer(64, 28672, seed=4)
+    plain = qw.synth_layer(256, 4096, seed=5)
+    assert qw.DeviceLayer(dense).uses_tensor_core
+    assert qw.DeviceLayer(wide).uses_tensor_core
+    assert not qw.DeviceLayer(plain).uses_tensor_core
+    assert not qw.DeviceLayer(dense, kernel="simt").uses_tensor_core
+    assert qw.DeviceLayer(plain, kernel="mma").uses_tensor_core
+    x = qw.synth_activation(13824, 6)
+    import torch
+    y = qw.DeviceLayer(dense).matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel_l2(y, oracle.matvec_f64(dense, x)) <= TOL
