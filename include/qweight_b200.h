@@ -249,6 +249,12 @@ int qw_debug_chain_timeline(const qw_chain* chain, unsigned long long* out, uint
  * (engine.cpp:124-132).  x_len must equal batch * cols. */
 int qw_matvec_host(const qw_layer* layer, const float* x, uint64_t x_len,
                    uint32_t batch, float* y, qw_workspace* ws, void* stream);
+/* Same with per-stage device times (MatvecResult.stage_ns, engine.hpp:19-23):
+ * stage_ns[0] = host->device copy of x, [1] = [2] = 0 (the 2-order scales and
+ * the decode are fused into the kernel), [3] = the fused kernel(s).  The x / y
+ * device buffers live in the workspace (grown once, reused). */
+int qw_matvec_host_ex(const qw_layer* layer, const float* x, uint64_t x_len, uint32_t batch,
+                      float* y, qw_workspace* ws, void* stream, uint64_t* stage_ns);
 
 /* reconstruct_dense (engine.hpp:26): w device fp32 [rows][padded_cols],
  * permuted order, bit-exact with the reference. */

@@ -74,6 +74,7 @@ class DeviceLayer {
     qw_layer_info info{};
     check(qw_layer_get_info(layer_, &info));
     padded_cols_ = info.padded_cols;
+    payload_ = info.payload_bytes;
   }
   DeviceLayer(const DeviceLayer&) = delete;
   DeviceLayer& operator=(const DeviceLayer&) = delete;
@@ -84,17 +85,22 @@ class DeviceLayer {
   uint32_t rows() const { return rows_; }
   uint32_t cols() const { return cols_; }
   uint32_t padded_cols() const { return padded_cols_; }
+  uint64_t payload_bytes() const { return payload_; }  // container.cpp:466-471
 
   // matvec_oracle / matvec_pipelined shape: host x in, MatvecResult out.
-  // stage_ns stays zero (one fused kernel has no CPU stage split); wall_ns
-  // is the host wall clock of the checked call, copies included.
+  // stage_ns (engine.hpp:19-23) on the GPU: [0] the host->device copy of x,
+  // [1] [2] 0 (the 2-order scales and the decode are fused into the kernel),
+  // [3] the fused kernel (CUDA events); wall_ns is the host wall clock of
+  // the checked call, copies included.
   MatvecResult matvec(std::span<const float> x) const {
     MatvecResult r;
     r.y.assign(rows_, 0.0f);
+    uint64_t st[4] = {0, 0, 0, 0};
     const auto t0 = std::chrono::steady_clock::now();
-    check(qw_matvec_host(layer_, x.data(), x.size(), 1, r.y.data(), ws_, nullptr));
+    check(qw_matvec_host_ex(layer_, x.data(), x.size(), 1, r.y.data(), ws_, nullptr, st));
     r.wall_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
                     std::chrono::steady_clock::now() - t0).count();
+    for (int k = 0; k < 4; ++k) r.stage_ns[k] = st[k];
     return r;
   }
   // reconstruct_dense: rows x padded_cols, permuted order, bit-exact
@@ -111,11 +117,44 @@ class DeviceLayer {
   qw_layer* layer_ = nullptr;
   qw_workspace* ws_ = nullptr;
   uint32_t rows_ = 0, cols_ = 0, padded_cols_ = 0;
+  uint64_t payload_ = 0;
 };
 
+// bench_matvec (engine.hpp:69-70, engine.cpp:317-350) on the B200: the two
+// modes the reference alternates become the two ways to call the GPU --
+// "oracle" = the device-resident call (x already in HBM, kernel time from
+// stage_ns[3]), "pipelined" = the checked host-buffer call (copies in,
+// wall clock).  Same BenchReport fields, bytes_touched and gflops.
+inline BenchReport bench_matvec(const DeviceLayer& dev, const PackedLayer& layer, std::span<const float> x,
+                                int repetitions, unsigned workers) {
+  if (repetitions < 1) throw qweight::Error("bench_matvec: repetitions must be >= 1");
+  if (workers == 0) throw qweight::Error("bench_matvec: workers must be >= 1");
+  BenchReport rep;
+  rep.rows = layer.cfg.rows;
+  rep.cols = layer.cfg.cols;
+  rep.workers = workers;
+  rep.repetitions = repetitions;
+  const uint64_t payload = dev.payload_bytes();
+  rep.avg_bit = 8.0 * (double)payload / ((double)layer.cfg.rows * layer.cfg.cols);
+  rep.bytes_touched = payload + 4ull * (layer.cfg.cols + layer.cfg.rows);
+  (void)dev.matvec(x);  // warm (bench_matvec warms too, engine.cpp:332-333)
+  for (int i = 0; i < repetitions; ++i) {
+    const MatvecResult r = dev.matvec(x);
+    rep.oracle_wall_ns += r.stage_ns[3];
+    rep.oracle_best_ns = i ? std::min(rep.oracle_best_ns, r.stage_ns[3]) : r.stage_ns[3];
+    rep.pipelined_wall_ns += r.wall_ns;
+    rep.pipelined_best_ns = i ? std::min(rep.pipelined_best_ns, r.wall_ns) : r.wall_ns;
+    for (int k = 0; k < 4; ++k) rep.oracle_stage_ns[k] += r.stage_ns[k], rep.pipelined_stage_ns[k] += r.stage_ns[k];
+  }
+  return rep;
+}
+
 // Free functions with the reference's exact signatures (engine.hpp:26-36).
-// Each call uploads the layer (validate_layer included); hold a DeviceLayer
-// to amortise the upload over many calls.
+// Each call uploads the layer (validate_layer, repack, cudaMalloc, ~7 MB of
+// H2D for a 4096^2 layer: measured by tests/native/shim_gpu.cpp, milliseconds
+// per call against microseconds for DeviceLayer::matvec).  They keep the
+// reference's value semantics (nothing is cached behind the caller's back);
+// hold a DeviceLayer to amortise the upload over many calls.
 inline WeightMatrix reconstruct_dense(const PackedLayer& layer) {
   return DeviceLayer(layer).reconstruct_dense();
 }

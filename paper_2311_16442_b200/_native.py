@@ -104,6 +104,8 @@ _SIGS = {
                                 C.c_void_p]),
     "qw_matvec_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
                                  C.c_void_p, C.c_void_p]),
+    "qw_matvec_host_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]),
     "qw_dequant": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "qw_unpack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_void_p]),

@@ -67,6 +67,13 @@ struct qw_chain {
 
 struct qw_workspace {
   qwdev::Workspace ws;
+  // host-buffer calls (qw_matvec_host*): device copies of x / y, grown on
+  // demand and reused (no allocation on the steady-state call path), and
+  // events for the per-stage device times
+  float* dx = nullptr;
+  float* dy = nullptr;
+  size_t dx_cap = 0, dy_cap = 0;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -653,6 +660,9 @@ int qw_workspace_free(qw_workspace* W) {
   if (!W) return QW_OK;
   cudaSetDevice(W->ws.device);
   cudaFree(W->ws.flags);
+  cudaFree(W->dx), cudaFree(W->dy);
+  for (auto& e : W->ev)
+    if (e) cudaEventDestroy(e);
   delete W;
   return QW_OK;
 }
@@ -674,6 +684,11 @@ int qw_matvec_pdl(const qw_layer* L, const float* x, uint32_t batch, float* y, q
 
 int qw_matvec_host(const qw_layer* L, const float* x, uint64_t x_len, uint32_t batch, float* y,
                    qw_workspace* ws, void* stream) {
+  return qw_matvec_host_ex(L, x, x_len, batch, y, ws, stream, nullptr);
+}
+
+int qw_matvec_host_ex(const qw_layer* L, const float* x, uint64_t x_len, uint32_t batch, float* y,
+                      qw_workspace* ws, void* stream, uint64_t* stage_ns) {
   if (int s = check_ws(L, ws, batch)) return s;
   if (!x || !y) return fail(QW_ERR_ARG, "matvec: null activation or output");
   // checked_permute (engine.cpp:124-132)
@@ -683,23 +698,42 @@ int qw_matvec_host(const qw_layer* L, const float* x, uint64_t x_len, uint32_t b
     if (!std::isfinite(x[i])) return fail(QW_ERR_ARG, "matvec: non-finite activation");
   cudaSetDevice(L->device);
   cudaStream_t st = (cudaStream_t)stream;
-  float *dx = nullptr, *dy = nullptr;
   const size_t xb = x_len * 4, yb = (size_t)batch * L->info.rows * 4;
   cudaError_t e;
-  if ((e = cudaMallocAsync((void**)&dx, xb, st)) != cudaSuccess) return cuda_fail(e, "alloc x");
-  if ((e = cudaMallocAsync((void**)&dy, yb, st)) != cudaSuccess) {
-    cudaFreeAsync(dx, st);
-    return cuda_fail(e, "alloc y");
+  if (xb > ws->dx_cap) {  // grow once, keep: the steady-state call allocates nothing
+    cudaFree(ws->dx);
+    ws->dx = nullptr, ws->dx_cap = 0;
+    if ((e = cudaMalloc((void**)&ws->dx, xb)) != cudaSuccess) return cuda_fail(e, "alloc x");
+    ws->dx_cap = xb;
   }
+  if (yb > ws->dy_cap) {
+    cudaFree(ws->dy);
+    ws->dy = nullptr, ws->dy_cap = 0;
+    if ((e = cudaMalloc((void**)&ws->dy, yb)) != cudaSuccess) return cuda_fail(e, "alloc y");
+    ws->dy_cap = yb;
+  }
+  if (stage_ns && !ws->ev[0])
+    for (auto& ev : ws->ev)
+      if ((e = cudaEventCreate(&ev)) != cudaSuccess) return cuda_fail(e, "event");
   int status = QW_OK;
-  if ((e = cudaMemcpyAsync(dx, x, xb, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+  if (stage_ns) cudaEventRecord(ws->ev[0], st);
+  if ((e = cudaMemcpyAsync(ws->dx, x, xb, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     status = cuda_fail(e, "copy x");
-  if (!status) status = run_matvec(L, dx, batch, dy, ws, stream, false);
-  if (!status && (e = cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+  if (stage_ns) cudaEventRecord(ws->ev[1], st);
+  if (!status) status = run_matvec(L, ws->dx, batch, ws->dy, ws, stream, false);
+  if (stage_ns) cudaEventRecord(ws->ev[2], st);
+  if (!status && (e = cudaMemcpyAsync(y, ws->dy, yb, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
     status = cuda_fail(e, "copy y");
-  cudaFreeAsync(dx, st);
-  cudaFreeAsync(dy, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess && !status) status = cuda_fail(e, "sync");
+  if (stage_ns && !status) {
+    // MatvecResult.stage_ns (engine.hpp:19-23) on the GPU: [0] the x copy
+    // (activation fetch), [1] [2] 0 (scales and decode are fused into the
+    // kernel), [3] the fused kernel(s)
+    float ms0 = 0.f, ms1 = 0.f;
+    cudaEventElapsedTime(&ms0, ws->ev[0], ws->ev[1]);
+    cudaEventElapsedTime(&ms1, ws->ev[1], ws->ev[2]);
+    stage_ns[0] = (uint64_t)(ms0 * 1e6), stage_ns[1] = 0, stage_ns[2] = 0, stage_ns[3] = (uint64_t)(ms1 * 1e6);
+  }
   return status;
 }
 

@@ -70,9 +70,9 @@ def default_workspace(device: int) -> Workspace:
 
 @dataclass
 class MatvecResult:
-    """MatvecResult (engine.hpp:19-23): y plus timing.  stage_ns holds the
-    device time of the fused kernel in slot 3 (there are no separate stages
-    on the GPU: fetch/scale/decode/FMA are one kernel)."""
+    """MatvecResult (engine.hpp:19-23): y plus timing.  stage_ns: [0] the
+    host->device copy of x, [1] [2] 0 (the 2-order scales and the decode are
+    fused into the kernel), [3] the fused kernel (CUDA events)."""
     y: np.ndarray
     stage_ns: list = field(default_factory=lambda: [0, 0, 0, 0])
     wall_ns: int = 0
@@ -156,12 +156,14 @@ class DeviceLayer:
         batch = 1 if x.ndim == 1 else x.shape[0]
         y = np.empty((batch, self.rows), dtype=np.float32)
         ws = workspace or default_workspace(self.device)
+        stages = (C.c_uint64 * 4)()
         t0 = time.perf_counter_ns()
-        check(lib().qw_matvec_host(self._h, x.ctypes.data, x.size, batch, y.ctypes.data, ws._h,
-                                   C.c_void_p(_stream_handle())))
+        check(lib().qw_matvec_host_ex(self._h, x.ctypes.data, x.size, batch, y.ctypes.data, ws._h,
+                                      C.c_void_p(_stream_handle()), stages))
         wall = time.perf_counter_ns() - t0
-        return MatvecResult(y=y.reshape(-1) if x.ndim == 1 else y, wall_ns=wall,
-                            stage_ns=[0, 0, 0, wall])
+        # stage_ns: [x copy, 0, 0, fused kernel] (device event times; the
+        # scale and decode stages are fused into the kernel)
+        return MatvecResult(y=y.reshape(-1) if x.ndim == 1 else y, wall_ns=wall, stage_ns=list(stages))
 
     # ------------------------------------------------------------ bit-exact
     def reconstruct_dense(self, stream=None):
