@@ -321,7 +321,8 @@ def run_ours(args):
     stack.capture()
     stack.replay()
     torch.cuda.synchronize()
-    if rank == 0 and not os.environ.get("QW_DEBUG_MMA_DIAG"):  # diagnostics runs compute garbage
+    diag = os.environ.get("QW_DEBUG_KNOBS") == "1" and os.environ.get("QW_DEBUG_MMA_DIAG")
+    if rank == 0 and not diag:  # diagnostics runs (QW_DEBUG_MMA_DIAG) compute garbage
         import oracle
         for j in (0, 4, 6):
             y = stack.y_of(j).cpu().numpy().reshape(-1)

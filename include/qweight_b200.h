@@ -294,6 +294,13 @@ int qw_debug_gemm_timeline(const qw_layer* layer, const float* x, uint32_t batch
 
 /* Number of kernels one qw_matvec call launches. */
 int qw_launches_per_matvec(const qw_layer* layer, uint32_t batch);
+/* Diagnostics: the power of two P of the batched path's fp16 A tiles (each
+ * element is RN_fp16(w * 2^-P), w the reconstruct_dense weight). */
+int qw_debug_gemm_shift(const qw_layer* layer, int* shift);
+/* Diagnostic knobs (QW_NQ1, QW_GEMM_KS, ... DESIGN.md section 6): the value
+ * the library uses for `name` -- the environment is consulted only when
+ * QW_DEBUG_KNOBS=1, otherwise every knob is its default. */
+uint32_t qw_debug_knob(const char* name, uint32_t dflt);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -342,7 +342,7 @@ int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_w
     cudaError_t e = cudaSetDevice(L->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   }
-  static const bool no_gemm = std::getenv("QW_NO_GEMM") != nullptr;
+  static const bool no_gemm = qwdev::knob_str("QW_NO_GEMM") != nullptr;
   const uint32_t xflags = (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u;
   int e = 0;
   if (batch >= 2 && L->dev.gemm.ok && !no_gemm) {
@@ -1002,8 +1002,17 @@ int qw_debug_gemm_timeline(const qw_layer* L, const float* x, uint32_t batch, fl
 
 int qw_debug_timeline_events(void) { return (int)qwdev::kTimelineEvents; }
 
+uint32_t qw_debug_knob(const char* name, uint32_t dflt) { return name ? qwdev::knob(name, dflt) : dflt; }
+
+int qw_debug_gemm_shift(const qw_layer* L, int* shift) {
+  if (!L || !shift) return fail(QW_ERR_ARG, "gemm shift: null argument");
+  if (!L->dev.gemm.ok) return fail(QW_ERR_UNSUPPORTED, "gemm shift: layer has no batched tensor-core plan");
+  *shift = L->dev.gemm.shift;
+  return QW_OK;
+}
+
 int qw_launches_per_matvec(const qw_layer* L, uint32_t batch) {
-  if (L && batch >= 2 && L->dev.gemm.ok && !std::getenv("QW_NO_GEMM")) return 2;  // x prologue (+ CSR), GEMM
+  if (L && batch >= 2 && L->dev.gemm.ok && !qwdev::knob_str("QW_NO_GEMM")) return 2;  // x prologue (+ CSR), GEMM
   return (int)batch;
 }
 

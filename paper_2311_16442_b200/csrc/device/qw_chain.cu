@@ -667,7 +667,7 @@ int plan_chain(ChainPlan** out, const ChainStepDesc* steps, uint32_t n, int num_
     e = cudaMemcpy((uint8_t*)p->dmem + bytes_steps, hc.data(), sizeof(ChainCta) * hc.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
-  if (e == cudaSuccess && std::getenv("QW_CHAIN_WATCH")) {  // diagnostics: hang -> record + trap
+  if (e == cudaSuccess && qwdev::knob_str("QW_CHAIN_WATCH")) {  // diagnostics: hang -> record + trap
     static unsigned* host_watch = nullptr;
     if (!host_watch) {
       e = cudaHostAlloc((void**)&host_watch, 148 * 32 * 8 * 4 * 4, cudaHostAllocMapped);

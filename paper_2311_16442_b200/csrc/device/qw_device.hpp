@@ -24,8 +24,23 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace qwdev {
+
+// Diagnostic knobs (QW_NQ1, QW_WIDE, QW_GEMM_KS, ...): read from the
+// environment ONLY when QW_DEBUG_KNOBS=1 is set; otherwise every knob is its
+// default -- the product's behaviour does not depend on the environment
+// (tests/test_boundary.py pins this).
+inline const char* knob_str(const char* name) {
+  const char* gate = std::getenv("QW_DEBUG_KNOBS");
+  if (!gate || gate[0] != '1') return nullptr;
+  return std::getenv(name);
+}
+inline uint32_t knob(const char* name, uint32_t dflt) {
+  const char* e = knob_str(name);
+  return e ? (uint32_t)std::atoi(e) : dflt;
+}
 
 constexpr int kRowsPerQuad = 4;
 

@@ -49,6 +49,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "qw_device.hpp"
 #include "qw_ptx.cuh"
@@ -645,7 +646,7 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
   p.stages = G.T2 / 2;                               // MMA sub-stages per row
   p.wstages = (p.stages + kSubPerW - 1) / kSubPerW;  // weight stages per row
   p.ks = std::max<uint32_t>(1, std::min<uint32_t>(std::min<uint32_t>(p.wstages, 8u), (uint32_t)num_sms / p.tiles));
-  const char* force_ks = std::getenv("QW_GEMM_KS");  // diagnostics: force the cluster K split
+  const char* force_ks = qwdev::knob_str("QW_GEMM_KS");  // diagnostics: force the cluster K split
   if (force_ks)
     p.ks = std::max<uint32_t>(1, std::min<uint32_t>(std::min<uint32_t>(p.wstages, 8u), (uint32_t)std::atoi(force_ks)));
   // stream-K when it shortens the critical path: every SM takes an equal
@@ -654,7 +655,7 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
   {
     const uint32_t W = p.tiles * p.wstages, C = std::min<uint32_t>((uint32_t)num_sms, W);
     const uint32_t crit_ks = (p.wstages + p.ks - 1) / p.ks, crit_stream = (W + C - 1) / C;
-    if (!force_ks && !std::getenv("QW_GEMM_NOSTREAM") && p.stages % kSubPerW == 0 && p.tiles <= C &&
+    if (!force_ks && !qwdev::knob_str("QW_GEMM_NOSTREAM") && p.stages % kSubPerW == 0 && p.tiles <= C &&
         crit_stream < crit_ks) {
       auto first = [&](uint64_t i) { return (uint32_t)(((i + 1) * C - 1) / W); };
       uint32_t kmax = 0;
@@ -701,15 +702,20 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
   if ((e = cudaMalloc((void**)&p.xpt, (size_t)p.stages * kBStageBytes)) != cudaSuccess) return (int)e;
   if ((e = cudaMalloc((void**)&p.xexp, 16 * sizeof(int))) != cudaSuccess) return (int)e;
   if ((e = cudaMalloc((void**)&p.ycsr, (size_t)16 * G.rows * 4)) != cudaSuccess) return (int)e;
-  static bool attr = false;
-  if (!attr) {
+  // the opt-in limits are per device: one bit per device, set under a lock
+  static std::mutex attr_mu;
+  static uint64_t attr_dev = 0;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  std::lock_guard<std::mutex> lk(attr_mu);
+  if (cur >= 64 || !(attr_dev & (1ull << cur))) {
     for (const void* k : {(const void*)gemm_kernel<false>, (const void*)gemm_kernel<true>}) {
       if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem)) != cudaSuccess)
         return (int)e;
       if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
         return (int)e;
     }
-    attr = true;
+    if (cur < 64) attr_dev |= 1ull << cur;
   }
   p.ok = 1;
   return 0;
@@ -764,7 +770,7 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  static const bool no_pdl = std::getenv("QW_GEMM_NOPDL") != nullptr;  // diagnostics
+  static const bool no_pdl = qwdev::knob_str("QW_GEMM_NOPDL") != nullptr;  // diagnostics
   cfg.numAttrs = no_pdl ? 1 : 2;
   void* params[] = {&a};
   return (int)cudaLaunchKernelExC(&cfg, use_stream ? (const void*)gemm_kernel<true> : (const void*)gemm_kernel<false>,

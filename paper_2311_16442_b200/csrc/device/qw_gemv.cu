@@ -42,6 +42,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <cstdint>
 #include <type_traits>
 #include <vector>
@@ -775,7 +776,7 @@ namespace {
 int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_ptrs, const uint32_t* seg_rows,
               uint32_t n, int num_sms) {
   uint32_t per_sm = 1;
-  if (const char* e = std::getenv("QW_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
+  if (const char* e = qwdev::knob_str("QW_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
   uint64_t total = 0;
   uint32_t lq[kMaxSeg];
   for (uint32_t l = 0; l < n; ++l) lq[l] = (seg_rows[l] + kRowsPerQuad - 1) / kRowsPerQuad, total += lq[l];
@@ -894,8 +895,13 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
   p.x_first = env_u32("QW_XFIRST", alone ? 1u : 0u);
   p.x_gate = env_u32("QW_XGATE", alone ? 1u : 1000000u);
   p.pf_late = env_u32("QW_PF_LATE", 1);
-  static bool attr_set = false;  // raise the opt-in limit once per process
-  if (!attr_set) {
+  // raise the opt-in limit once per device (the attribute is per device)
+  static std::mutex attr_mu;
+  static uint64_t attr_dev = 0;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  std::lock_guard<std::mutex> lk(attr_mu);
+  if (cur >= 64 || !(attr_dev & (1ull << cur))) {
     for (bool uni : {false, true})
       for (bool xsm : {false, true})
         for (uint32_t k : {1u, 2u, 3u, 4u}) {
@@ -914,7 +920,7 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
                                              (int)(227 * 1024));
       if (err != cudaSuccess) return (int)err;
     }
-    attr_set = true;
+    if (cur < 64) attr_dev |= 1ull << cur;
   }
   return 0;
 }

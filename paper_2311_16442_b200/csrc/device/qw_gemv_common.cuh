@@ -141,7 +141,7 @@ __device__ __forceinline__ uint32_t win_base(uint32_t l) { return l * 20u + (l >
 
 // ------------------------------------------------------------ host helpers
 uint32_t env_u32(const char* name, uint32_t dflt) {
-  const char* e = std::getenv(name);
+  const char* e = knob_str(name);
   return e ? (uint32_t)std::atoi(e) : dflt;
 }
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }

@@ -39,6 +39,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "qw_device.hpp"
@@ -885,7 +886,7 @@ cudaError_t launch_ex(const void* fn, dim3 grid, dim3 block, size_t smem, cudaSt
 size_t align16(size_t v) { return (v + 15) / 16 * 16; }
 
 uint32_t diag_flags() {
-  static const char* d = std::getenv("QW_DEBUG_MMA_DIAG");
+  static const char* d = qwdev::knob_str("QW_DEBUG_MMA_DIAG");
   return d ? (uint32_t)std::atoi(d) : 0u;
 }
 
@@ -969,12 +970,14 @@ int make_layout(MmaLayout& L, uint32_t rec_stride, uint32_t cols, uint32_t items
 int opt_in_smem(const void* fn) {
   int dev = 0;
   cudaGetDevice(&dev);
-  static uint32_t done[2] = {0, 0};  // bit per device: the >48 KB opt-in is per device
+  static std::mutex mu;
+  static uint64_t done[2] = {0, 0};  // bit per device: the >48 KB opt-in is per device
   const int which = fn == (const void*)mma_gemv_kernel ? 0 : 1;
-  if (dev < 32 && !(done[which] & (1u << dev))) {
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 64 || !(done[which] & (1ull << dev))) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return (int)e;
-    done[which] |= 1u << dev;
+    if (dev < 64) done[which] |= 1ull << dev;
   }
   return 0;
 }
@@ -1110,7 +1113,7 @@ int plan_mma_chain(MmaChainPlan** out, const ChainStepDesc* steps, uint32_t n, i
   // the largest, the producer addresses records with the layer's stride
   const size_t b_steps = sizeof(MmaStepDesc) * n, b_ranges = sizeof(MmaCtaRange) * rg.size();
   const size_t b_prod = sizeof(MmaProdStep) * pd.size(), b_done = 4 * n;
-  const char* tle = std::getenv("QW_DEBUG_MMA_TL");
+  const char* tle = qwdev::knob_str("QW_DEBUG_MMA_TL");
   const size_t b_tl = (tle && tle[0] == '1') ? (size_t)n * grid * 8 * 8 : 0;
   cudaError_t e = cudaMalloc(&P->dmem, b_steps + b_ranges + b_prod + b_done + 64 + b_tl);
   if (e != cudaSuccess) return (int)e;

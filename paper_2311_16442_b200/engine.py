@@ -137,11 +137,19 @@ class DeviceLayer:
         xb = x.reshape(1, -1) if squeeze else x
         if xb.dtype != torch.float32 or not xb.is_cuda or not xb.is_contiguous():
             raise QWeightError(1, "matvec: x must be a contiguous cuda float32 tensor")
+        if xb.device.index != self.device:
+            raise QWeightError(1, f"matvec: x is on cuda:{xb.device.index}, the layer on cuda:{self.device}")
         batch = xb.shape[0]
         if xb.shape[1] != self.cols:
             raise QWeightError(1, "matvec: activation length != input channels")
         if out is None:
             out = torch.empty((batch, self.rows), dtype=torch.float32, device=xb.device)
+        elif (out.dtype != torch.float32 or not out.is_cuda or not out.is_contiguous() or
+              out.numel() != batch * self.rows or out.device != xb.device):
+            # the kernel writes y[n * rows + row] from out.data_ptr(): anything
+            # but a contiguous fp32 [batch, rows] buffer on x's device is wrong
+            raise QWeightError(1, "matvec: out must be a contiguous cuda float32 tensor of batch * rows "
+                                  "elements on the activation's device")
         ws = workspace or default_workspace(self.device)
         flags = (1 if pdl else 0) | (2 if x_independent else 0)
         check(lib().qw_matvec_ex(self._h, C.c_void_p(xb.data_ptr()), batch,

@@ -6,18 +6,19 @@ then the packed layer is sharded:
 
 * column-parallel ("col", Megatron q/k/v/gate/up): rank r owns output rows
   [r OC/N, (r+1) OC/N) in whole 2-order row blocks (qw_host_shard_rows); every
-  rank reads the full x, computes its rows, and an NCCL all-gather assembles y.
+  rank reads the full x, computes its rows, and an all-gather assembles y.
 * row-parallel ("row", Megatron o/down): rank r owns a contiguous range of
   paired tiles (qw_host_shard_tiles: the tiles' 2-bit triples, 4-bit blocks,
   2-order columns and CSR entries, rebased); its input is the slice of the
-  permuted activation those tiles read, and an NCCL all-reduce (sum) of the
+  permuted activation those tiles read, and an all-reduce (sum) of the
   partial y gives y.
 
-One process per GPU (torch.distributed, backend "nccl"); the local GEMV is
-the fused K2 kernel (batch 1) or K4 (batch 2..16).  The same class runs on
-CPU with backend "gloo" and the C oracle as the local matvec (test only:
-`local="oracle"`), which is how the sharding + collective logic is tested
-without GPUs.
+One process per GPU (torch.distributed); the local GEMV is always this
+repository's kernel on the rank's GPU (K2 / K2m at batch 1, K4 at batch
+2..16).  The collective runs on the device tensors with NCCL; with a gloo
+group (the CPU test harness, several ranks sharing one GPU) the same code
+stages the collective's buffers through host memory -- the sharding, gather
+and reduction logic is identical.
 """
 from __future__ import annotations
 
@@ -40,80 +41,77 @@ def split_tiles(tiles: int, world: int) -> list[tuple[int, int]]:
     return [(tiles * r // world, tiles * (r + 1) // world) for r in range(world)]
 
 
+def shard_layer(layer: PackedLayer, rank: int, world: int, mode: str):
+    """The rank's shard of a globally quantized layer.  col: (shard, row
+    ranges of every rank, None); row: (shard, None, idx) where idx[i] is the
+    original channel shard channel i reads (-1 for a pad: reads 0)."""
+    if mode not in ("col", "row"):
+        raise ValueError("mode must be 'col' or 'row'")
+    if mode == "col":
+        ranges = split_rows(layer.cfg.rows, layer.cfg.group2, world)
+        r0, r1 = ranges[rank]
+        return shard_rows(layer, r0, r1), ranges, None
+    if layer.cfg.tail2_blocks or layer.cfg.tail4_blocks:
+        raise ValueError("row-parallel split needs paired tiles (T2 == T4)")
+    t0, t1 = split_tiles(layer.cfg.triples, world)[rank]
+    shard, slots = shard_tiles(layer, t0, t1)
+    perm = layer.plan_perm.astype(np.int64)[slots]
+    return shard, None, np.where(perm == PAD, -1, perm)
+
+
 class TPLinear:
     """One rank's shard of a quantized linear + the collective that completes it."""
 
     def __init__(self, layer: PackedLayer, rank: int, world: int, mode: str, device=None,
-                 local: str = "gpu"):
-        if mode not in ("col", "row"):
-            raise ValueError("mode must be 'col' or 'row'")
-        self.mode, self.rank, self.world, self.local = mode, rank, world, local
+                 kernel: str = "auto"):
+        import torch
+
+        from .engine import DeviceLayer
+        self.mode, self.rank, self.world = mode, rank, world
         self.rows, self.cols = layer.cfg.rows, layer.cfg.cols
-        if mode == "col":
-            self.ranges = split_rows(self.rows, layer.cfg.group2, world)
-            r0, r1 = self.ranges[rank]
-            self.shard = shard_rows(layer, r0, r1)
-            self.idx = None
-        else:
-            if layer.cfg.tail2_blocks or layer.cfg.tail4_blocks:
-                raise ValueError("row-parallel split needs paired tiles (T2 == T4)")
-            t0, t1 = split_tiles(layer.cfg.triples, world)[rank]
-            self.shard, slots = shard_tiles(layer, t0, t1)
-            perm = layer.plan_perm.astype(np.int64)[slots]
-            # shard channel i reads original channel perm[i]; pads read 0
-            self.idx = np.where(perm == PAD, -1, perm)
-        self.dev = None
-        if local == "gpu":
-            import torch
+        self.shard, self.ranges, self.idx = shard_layer(layer, rank, world, mode)
+        self.torch = torch
+        dev = torch.device(device if device is not None else "cuda")
+        index = dev.index if dev.index is not None else torch.cuda.current_device()
+        self.device = torch.device("cuda", index)
+        self.dl = DeviceLayer(self.shard, index, kernel=kernel)
+        if self.idx is not None:
+            # one gather from x padded with a zero column: pads read it
+            self.gidx = torch.from_numpy(np.where(self.idx >= 0, self.idx, self.cols)).to(self.device)
+        self.max_rows = max(r1 - r0 for r0, r1 in self.ranges) if mode == "col" else self.rows
 
-            from .engine import DeviceLayer
-            self.torch = torch
-            self.device = torch.device(device if device is not None else "cuda")
-            self.dl = DeviceLayer(self.shard, self.device.index or 0)
-            if self.idx is not None:
-                real = self.idx >= 0
-                self.gidx = torch.from_numpy(np.where(real, self.idx, 0)).to(self.device)
-                self.gmask = torch.from_numpy(real.astype(np.float32)).to(self.device)
-            self.max_rows = max(r1 - r0 for r0, r1 in self.ranges) if mode == "col" else self.rows
+    def _collective(self, fn, *tensors, group=None):
+        """Run a collective on device tensors (NCCL) or, for a gloo group,
+        through host copies (the multi-rank CPU harness)."""
+        import torch.distributed as dist
+        if dist.get_backend(group) == "nccl":
+            fn(*tensors)
+            return tensors
+        host = [t.cpu() if isinstance(t, self.torch.Tensor) else [u.cpu() for u in t] for t in tensors]
+        fn(*host)
+        return host
 
-    # ------------------------------------------------------------------ GPU
     def forward(self, x, group=None):
         """x: full activation(s) in original channel order, cuda fp32
-        [cols] or [batch, cols], identical on every rank.  Returns the full y."""
+        [cols] or [batch, cols], identical on every rank.  Returns the full y
+        on the rank's device."""
         torch = self.torch
         import torch.distributed as dist
         squeeze = x.dim() == 1
-        xb = x.reshape(1, -1) if squeeze else x
+        xb = (x.reshape(1, -1) if squeeze else x).to(self.device)
         b = xb.shape[0]
         if self.mode == "col":
             r0, r1 = self.ranges[self.rank]
             y_loc = torch.zeros(b, self.max_rows, dtype=torch.float32, device=self.device)
-            self.dl.matvec(xb, out=y_loc[:, : r1 - r0])
-            gathered = torch.empty(self.world, b, self.max_rows, dtype=torch.float32, device=self.device)
-            dist.all_gather_into_tensor(gathered, y_loc, group=group)
-            y = torch.cat([gathered[r, :, : e - s] for r, (s, e) in enumerate(self.ranges)], dim=1)
+            y_loc[:, : r1 - r0] = self.dl.matvec(xb)  # contiguous [b, r1 - r0] first
+            gathered = torch.empty(self.world * b, self.max_rows, dtype=torch.float32, device=self.device)
+            out = self._collective(lambda o, i: dist.all_gather_into_tensor(o, i, group=group),
+                                   gathered, y_loc, group=group)[0]
+            out = out.to(self.device).reshape(self.world, b, self.max_rows)
+            y = torch.cat([out[r, :, : e - s] for r, (s, e) in enumerate(self.ranges)], dim=1)
         else:
-            xs = (xb.index_select(1, self.gidx) * self.gmask).contiguous()
-            y = self.dl.matvec(xs)
-            dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
+            xp = torch.cat([xb, torch.zeros(b, 1, dtype=xb.dtype, device=self.device)], dim=1)
+            y = self.dl.matvec(xp.index_select(1, self.gidx))
+            y = self._collective(lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group),
+                                 y, group=group)[0].to(self.device)
         return y.reshape(-1) if squeeze else y
-
-    # ------------------------------------------------------------------ CPU (tests)
-    def forward_oracle(self, x: np.ndarray, group=None) -> np.ndarray:
-        """Same split + collectives with the C oracle as the local matvec
-        (gloo on CPU).  Test infrastructure: imports oracle lazily."""
-        import torch
-        import torch.distributed as dist
-
-        import oracle
-        if self.mode == "col":
-            r0, r1 = self.ranges[self.rank]
-            local = np.zeros(max(e - s for s, e in self.ranges), np.float32)
-            local[: r1 - r0] = oracle.matvec_oracle(self.shard, x)
-            parts = [torch.zeros_like(torch.from_numpy(local)) for _ in range(self.world)]
-            dist.all_gather(parts, torch.from_numpy(local), group=group)
-            return np.concatenate([parts[r].numpy()[: e - s] for r, (s, e) in enumerate(self.ranges)])
-        xs = np.where(self.idx >= 0, x[np.maximum(self.idx, 0)], 0.0).astype(np.float32)
-        part = torch.from_numpy(oracle.matvec_f64(self.shard, xs).astype(np.float64))
-        dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
-        return part.numpy()

@@ -1,5 +1,5 @@
 """Per-step phase timeline of the tensor-core decode-chain kernel.
-usage: QW_DEBUG_MMA_TL=1 python scripts/chain_tl.py [decoder_layers] [indep]
+usage: QW_DEBUG_KNOBS=1 QW_DEBUG_MMA_TL=1 python scripts/chain_tl.py [decoder_layers] [indep]
 Prints, per step kind (q/k/v, o, gate/up, down), the median over CTAs and
 steps of each phase (µs): dependency wait, x staging + B build, items, CSR
 meet, reduction, release; and the step period."""
@@ -18,13 +18,14 @@ import paper_2311_16442_b200 as qw  # noqa: E402
 from paper_2311_16442_b200._native import lib  # noqa: E402
 from paper_2311_16442_b200.stack import LinearStack  # noqa: E402
 
-assert os.environ.get("QW_DEBUG_MMA_TL") == "1", "set QW_DEBUG_MMA_TL=1"
+assert os.environ.get("QW_DEBUG_MMA_TL") == "1" and os.environ.get("QW_DEBUG_KNOBS") == "1", \
+    "set QW_DEBUG_KNOBS=1 QW_DEBUG_MMA_TL=1"
 NL = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 indep = len(sys.argv) > 2 and sys.argv[2] == "indep"
 cache = Path(os.environ.get("QW_BENCH_CACHE", Path(tempfile.gettempdir()) / "qw_bench_cache"))
 cache.mkdir(parents=True, exist_ok=True)
 base = bench.make_layers(0, 1, cache, os.cpu_count() or 1)
-dls = [qw.DeviceLayer(L, 0) for L in base]
+dls = [qw.DeviceLayer(L, 0, kernel="mma") for L in base]
 per = []
 for l in range(NL):
     for i, d in enumerate(dls):

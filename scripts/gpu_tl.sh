@@ -1,6 +1,6 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 timeout 600 python scripts/batch_sweep.py > gpurun_out/batch_sweep_v17.jsonl 2>/dev/null
-QW_GEMM_NOSTREAM=1 timeout 600 python scripts/batch_sweep.py 24 2>/dev/null | python -c "
+QW_DEBUG_KNOBS=1 QW_GEMM_NOSTREAM=1 timeout 600 python scripts/batch_sweep.py 24 2>/dev/null | python -c "
 import json,sys
 for l in sys.stdin:
     d=json.loads(l)

@@ -82,3 +82,21 @@ def test_cpp_shim_compiles_against_reference_headers(tmp_path):
                    check=True)
     # workers == 0 throws qweight::Error before touching the device (engine.cpp:187-188)
     assert subprocess.run([str(exe)]).returncode == 0
+
+
+def test_diagnostic_knobs_are_inert_without_the_debug_gate():
+    """The library reads its diagnostic knobs (QW_NQ1, QW_GEMM_KS, ...) only
+    under QW_DEBUG_KNOBS=1: the product's behaviour never depends on the
+    environment.  Checked in fresh processes."""
+    import os
+    import subprocess
+    import sys
+    code = ("import paper_2311_16442_b200 as qw; L = qw.lib(); "
+            "print(L.qw_debug_knob(b'QW_NQ1', 2), L.qw_debug_knob(b'QW_GEMM_KS', 0), "
+            "L.qw_debug_knob(b'QW_TEAMS_MIN_NQ', 4))")
+    env = {k: v for k, v in os.environ.items() if k != "QW_DEBUG_KNOBS"}
+    env.update(QW_NQ1="1", QW_GEMM_KS="3", QW_TEAMS_MIN_NQ="9")
+    run = lambda e: subprocess.run([sys.executable, "-c", code], env=e, cwd=str(ROOT), capture_output=True,  # noqa: E731
+                                   text=True, check=True).stdout.split()
+    assert run(env) == ["2", "0", "4"]          # defaults pinned
+    assert run({**env, "QW_DEBUG_KNOBS": "1"}) == ["1", "3", "9"]  # the gate opens them

@@ -249,6 +249,7 @@ def test_tp_linear_single_rank_nccl(mode):
     x = qw.synth_activation(1024, 10)
     try:
         tp = TPLinear(layer, 0, 1, mode, device="cuda:0")
+        assert tp.device == torch.device("cuda", 0)
         y = tp.forward(torch.from_numpy(x).cuda()).cpu().numpy()
         assert rel_l2(y, oracle.matvec_f64(layer, x)) <= TOL
     finally:
@@ -428,3 +429,41 @@ def test_auto_kernel_policy():
     import torch
     y = qw.DeviceLayer(dense).matvec(torch.from_numpy(x).cuda()).cpu().numpy()
     assert rel_l2(y, oracle.matvec_f64(dense, x)) <= TOL
+
+
+@pytest.mark.parametrize("rows,cols,ratio", [(256, 512, 0.01), (512, 4096, 0.005)])
+def test_k4_a_tile_is_the_rounded_reference_weight(rows, cols, ratio):
+    """every fp16 element of a K4 A tile is RN_fp16 of the
+    reference's fp32 weight (reconstruct_dense) times 2^-P.  With a one-hot
+    activation at permuted slot k, column n of the batched GEMM is exactly
+    A[:, k] * 2^P (one exact product, power-of-two column scales) plus the
+    slot's CSR outliers (exact), so y must equal f16(w[:, k] 2^-P) 2^P + csr
+    bit for bit."""
+    import ctypes as C
+    torch = _torch()
+    layer = qw.synth_layer(rows, cols, seed=rows + 7, outlier_ratio=ratio)
+    dl = qw.DeviceLayer(layer)
+    assert dl.launches_per_matvec(8) == 2, "expected the tcgen05 path"
+    P = C.c_int()
+    assert qw.lib().qw_debug_gemm_shift(dl._h, C.byref(P)) == 0
+    w = oracle.reconstruct_dense(layer)  # rows x padded_cols, permuted order
+    perm = layer.plan_perm.astype(np.int64)
+    real = np.nonzero(perm != qw.PAD)[0]
+    rng = np.random.default_rng(rows)
+    slots = np.concatenate([real[:3], rng.choice(real, 5, replace=False)])  # 2-bit and 4-bit slots
+    xs = np.zeros((len(slots), cols), np.float32)
+    for n, k in enumerate(slots):
+        xs[n, perm[k]] = 1.0
+    Y = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
+    rp, ci = layer.row_ptr.astype(np.int64), layer.col_ind.astype(np.int64)
+    vals = layer.values.view(np.float16).astype(np.float32)
+    scale = np.float32(2.0) ** np.float32(P.value)
+    for n, k in enumerate(slots):
+        a = (w[:, k] / scale).astype(np.float16).astype(np.float32) * scale  # RN_fp16(w 2^-P) 2^P
+        csr = np.zeros(rows, np.float32)
+        for r in range(rows):
+            hit = np.nonzero(ci[rp[r]:rp[r + 1]] == k)[0]
+            if hit.size:
+                csr[r] = vals[rp[r] + hit[0]]
+        expect = a + csr
+        assert np.array_equal(Y[n].view(np.uint32), expect.view(np.uint32)), (n, int(k))
