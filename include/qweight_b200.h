@@ -165,6 +165,14 @@ int qw_layer_upload(const qw_layer_view* view, int device, qw_layer** out);
 #define QW_UPLOAD_TENSOR_CORE 1u
 #define QW_UPLOAD_SIMT 2u
 int qw_layer_upload_ex(const qw_layer_view* view, int device, uint32_t flags, qw_layer** out);
+/* A QWL1 container (container.cpp:321-471: header, section table, CRC32)
+ * straight to the device: the bytes (e.g. an mmap'ed file) are parsed,
+ * CRC-checked and validated (validate_layer) on the host and repacked into
+ * the device formats, with no host PackedLayer handed back to the caller.
+ * QW_ERR_FORMAT for a corrupt container (deserialize_packed_layer's errors). */
+int qw_layer_upload_qwl(const uint8_t* bytes, uint64_t len, int device, uint32_t flags, qw_layer** out);
+/* Same from a file path (read_packed_layer, container.hpp:50-58). */
+int qw_layer_load(const char* path, int device, uint32_t flags, qw_layer** out);
 int qw_layer_free(qw_layer* layer);
 int qw_layer_get_info(const qw_layer* layer, qw_layer_info* info);
 /* 1 when batch-1 calls of the layer run K2m (the warp-MMA kernel), 0 for K2. */

@@ -82,6 +82,8 @@ _SIGS = {
     "qw_layer_upload": (C.c_int, [C.POINTER(LayerView), C.c_int, C.POINTER(C.c_void_p)]),
     "qw_layer_upload_ex": (C.c_int, [C.POINTER(LayerView), C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]),
     "qw_layer_uses_tensor_core": (C.c_int, [C.c_void_p]),
+    "qw_layer_upload_qwl": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "qw_layer_load": (C.c_int, [C.c_char_p, C.c_int, C.c_uint32, C.POINTER(C.c_void_p)]),
     "qw_layer_free": (C.c_int, [C.c_void_p]),
     "qw_layer_get_info": (C.c_int, [C.c_void_p, C.POINTER(LayerInfo)]),
     "qw_workspace_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),

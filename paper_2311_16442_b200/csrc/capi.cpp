@@ -360,6 +360,82 @@ int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_w
   return QW_OK;
 }
 
+int upload_packed(const qwb::PackedLayer& L, int device, uint32_t flags, qw_layer** out) {
+  {
+    qwb::validate_layer(L);
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) return fail(QW_ERR_CUDA, "upload: no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(QW_ERR_ARG, "upload: device index out of range");
+    if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    auto H = std::make_unique<qw_layer>();
+    H->device = device;
+    cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, device);
+    H->dev.g = geometry_of(L.cfg, L.csr.nnz());
+    fill_info(L.cfg, L.csr.nnz(), &H->info);
+    std::vector<uint8_t> quads;
+    std::vector<uint32_t> sorder, csr;
+    repack(L, H->dev.g, quads, sorder, csr);
+    csr.resize(csr.size() + 4, 0u);  // padding: 16-byte aligned bulk copies of a CTA's entries may overrun
+    std::vector<uint16_t> perm16(L.plan.perm.size());
+    for (size_t i = 0; i < perm16.size(); ++i)
+      perm16[i] = L.plan.perm[i] == qwb::kPad ? (uint16_t)L.cfg.cols : (uint16_t)L.plan.perm[i];  // pads: x[cols] = 0 slot
+    H->host_row_ptr = L.csr.row_ptr;
+    if (H->host_row_ptr.empty()) H->host_row_ptr.assign((size_t)L.cfg.rows + 1, 0u);
+    if (int pe = qwdev::plan_gemv(H->dev, H->num_sms, H->host_row_ptr.data())) {
+      if (pe == (int)cudaErrorInvalidConfiguration)
+        return fail(QW_ERR_UNSUPPORTED, "upload: layer too wide for the fused GEMV (at most 60 "
+                                        "chunks of 32 groups, i.e. about 30720 input channels)");
+      return cuda_fail((cudaError_t)pe, "gemv plan");
+    }
+    {  // 2^-P so that 15 * max|scale2| * 2^-P lies in [2^14, 2^15): fp16 1st-order scales
+      float mx = 0.0f;
+      for (const auto& sp : L.sorder) mx = std::max(mx, std::fabs(qwb::f16_to_f32(sp.scale2)));
+      int P = 0;
+      if (mx > 0.0f && std::isfinite(mx)) P = std::ilogb(15.0f * mx) - 14;
+      H->dev.plan.s_scale = std::ldexp(1.0f, -std::max(-100, std::min(100, P)));
+      H->max_scale2 = mx;
+      float m4 = 0.0f;
+      for (const auto& fb : L.fourbit) m4 = std::max(m4, std::fabs(qwb::f16_to_f32(fb.scale)));
+      H->max_s4 = m4;
+    }
+    if ((e = upload(&H->dev.quads, quads)) != cudaSuccess ||
+        (e = upload(&H->dev.sorder, sorder)) != cudaSuccess ||
+        (e = upload(&H->dev.perm, L.plan.perm)) != cudaSuccess ||
+        (e = upload(&H->dev.row_ptr, L.csr.row_ptr)) != cudaSuccess ||
+        (e = upload(&H->dev.csr, csr)) != cudaSuccess ||
+        (e = upload(&H->dev.perm16, perm16)) != cudaSuccess) {
+      free_dev(H->dev);
+      return cuda_fail(e, "upload");
+    }
+    if (int ge = qwdev::plan_gemm(H->dev, H->num_sms, H->max_scale2, H->max_s4)) {
+      free_dev(H->dev);
+      return cuda_fail((cudaError_t)ge, "gemm plan");
+    }
+    qwdev::mma_geometry(H->dev.mg, H->dev.g);
+    // batch-1 kernel policy (header): auto picks K2m where K2's plan falls
+    // back to the global-memory CSR loop or exceeds two groups per lane
+    const auto& gp = H->dev.plan;
+    const bool k2_slow = (L.csr.nnz() > 0 && !gp.csr_stage) || (gp.kmax > 2 && !gp.wide) || !gp.xsm;
+    const bool want_mma = (flags & QW_UPLOAD_TENSOR_CORE) || (!(flags & QW_UPLOAD_SIMT) && k2_slow);
+    if (H->dev.mg.ok && want_mma) {
+      std::vector<uint8_t> recs;
+      qwb::repack_mma(L, H->dev.mg, H->dev.plan.s_scale, recs);
+      const qwdev::DeviceLayer* one[1] = {&H->dev};
+      if ((e = upload(&H->dev.mrecs, recs)) != cudaSuccess || (e = alloc_mma_scratch(H->dev)) != cudaSuccess) {
+        free_dev(H->dev);
+        return cuda_fail(e, "upload (mma tiles)");
+      }
+      const uint32_t* rp[1] = {H->host_row_ptr.data()};
+      if (int pe = qwdev::plan_mma(H->dev.mplan, one, rp, 1, H->num_sms)) {
+        free_dev(H->dev);
+        return cuda_fail((cudaError_t)pe, "mma plan");
+      }
+    }
+    *out = H.release();
+    return (int)QW_OK;
+  }
+}
 }  // namespace
 
 extern "C" {
@@ -546,81 +622,29 @@ int qw_layer_upload(const qw_layer_view* v, int device, qw_layer** out) {
 int qw_layer_upload_ex(const qw_layer_view* v, int device, uint32_t flags, qw_layer** out) {
   return guarded([&] {
     if (!v || !out) return fail(QW_ERR_ARG, "upload: null argument");
-    const qwb::PackedLayer L = from_view(*v);
-    qwb::validate_layer(L);
-    int ndev = 0;
-    cudaError_t e = cudaGetDeviceCount(&ndev);
-    if (e != cudaSuccess || ndev == 0) return fail(QW_ERR_CUDA, "upload: no CUDA device available");
-    if (device < 0 || device >= ndev) return fail(QW_ERR_ARG, "upload: device index out of range");
-    if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
-    auto H = std::make_unique<qw_layer>();
-    H->device = device;
-    cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, device);
-    H->dev.g = geometry_of(L.cfg, L.csr.nnz());
-    fill_info(L.cfg, L.csr.nnz(), &H->info);
-    std::vector<uint8_t> quads;
-    std::vector<uint32_t> sorder, csr;
-    repack(L, H->dev.g, quads, sorder, csr);
-    csr.resize(csr.size() + 4, 0u);  // padding: 16-byte aligned bulk copies of a CTA's entries may overrun
-    std::vector<uint16_t> perm16(L.plan.perm.size());
-    for (size_t i = 0; i < perm16.size(); ++i)
-      perm16[i] = L.plan.perm[i] == qwb::kPad ? (uint16_t)L.cfg.cols : (uint16_t)L.plan.perm[i];  // pads: x[cols] = 0 slot
-    H->host_row_ptr = L.csr.row_ptr;
-    if (H->host_row_ptr.empty()) H->host_row_ptr.assign((size_t)L.cfg.rows + 1, 0u);
-    if (int pe = qwdev::plan_gemv(H->dev, H->num_sms, H->host_row_ptr.data())) {
-      if (pe == (int)cudaErrorInvalidConfiguration)
-        return fail(QW_ERR_UNSUPPORTED, "upload: layer too wide for the fused GEMV (at most 60 "
-                                        "chunks of 32 groups, i.e. about 30720 input channels)");
-      return cuda_fail((cudaError_t)pe, "gemv plan");
-    }
-    {  // 2^-P so that 15 * max|scale2| * 2^-P lies in [2^14, 2^15): fp16 1st-order scales
-      float mx = 0.0f;
-      for (const auto& sp : L.sorder) mx = std::max(mx, std::fabs(qwb::f16_to_f32(sp.scale2)));
-      int P = 0;
-      if (mx > 0.0f && std::isfinite(mx)) P = std::ilogb(15.0f * mx) - 14;
-      H->dev.plan.s_scale = std::ldexp(1.0f, -std::max(-100, std::min(100, P)));
-      H->max_scale2 = mx;
-      float m4 = 0.0f;
-      for (const auto& fb : L.fourbit) m4 = std::max(m4, std::fabs(qwb::f16_to_f32(fb.scale)));
-      H->max_s4 = m4;
-    }
-    if ((e = upload(&H->dev.quads, quads)) != cudaSuccess ||
-        (e = upload(&H->dev.sorder, sorder)) != cudaSuccess ||
-        (e = upload(&H->dev.perm, L.plan.perm)) != cudaSuccess ||
-        (e = upload(&H->dev.row_ptr, L.csr.row_ptr)) != cudaSuccess ||
-        (e = upload(&H->dev.csr, csr)) != cudaSuccess ||
-        (e = upload(&H->dev.perm16, perm16)) != cudaSuccess) {
-      free_dev(H->dev);
-      return cuda_fail(e, "upload");
-    }
-    if (int ge = qwdev::plan_gemm(H->dev, H->num_sms, H->max_scale2, H->max_s4)) {
-      free_dev(H->dev);
-      return cuda_fail((cudaError_t)ge, "gemm plan");
-    }
-    qwdev::mma_geometry(H->dev.mg, H->dev.g);
-    // batch-1 kernel policy (header): auto picks K2m where K2's plan falls
-    // back to the global-memory CSR loop or exceeds two groups per lane
-    const auto& gp = H->dev.plan;
-    const bool k2_slow = (L.csr.nnz() > 0 && !gp.csr_stage) || (gp.kmax > 2 && !gp.wide) || !gp.xsm;
-    const bool want_mma = (flags & QW_UPLOAD_TENSOR_CORE) || (!(flags & QW_UPLOAD_SIMT) && k2_slow);
-    if (H->dev.mg.ok && want_mma) {
-      std::vector<uint8_t> recs;
-      qwb::repack_mma(L, H->dev.mg, H->dev.plan.s_scale, recs);
-      const qwdev::DeviceLayer* one[1] = {&H->dev};
-      if ((e = upload(&H->dev.mrecs, recs)) != cudaSuccess || (e = alloc_mma_scratch(H->dev)) != cudaSuccess) {
-        free_dev(H->dev);
-        return cuda_fail(e, "upload (mma tiles)");
-      }
-      const uint32_t* rp[1] = {H->host_row_ptr.data()};
-      if (int pe = qwdev::plan_mma(H->dev.mplan, one, rp, 1, H->num_sms)) {
-        free_dev(H->dev);
-        return cuda_fail((cudaError_t)pe, "mma plan");
-      }
-    }
-    *out = H.release();
-    return (int)QW_OK;
+    return upload_packed(from_view(*v), device, flags, out);
   });
 }
+
+// QWL1 container (container.cpp:321-471) straight to the device: parse +
+// CRC + validate_layer on the host, no intermediate host object for the caller
+int qw_layer_upload_qwl(const uint8_t* bytes, uint64_t len, int device, uint32_t flags, qw_layer** out) {
+  return guarded([&] {
+    if (!bytes || !out) return fail(QW_ERR_ARG, "upload qwl: null argument");
+    return upload_packed(qwb::deserialize_layer(std::span<const uint8_t>(bytes, len)), device, flags, out);
+  });
+}
+
+int qw_layer_load(const char* path, int device, uint32_t flags, qw_layer** out) {
+  return guarded([&] {
+    if (!path || !out) return fail(QW_ERR_ARG, "load: null argument");
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return fail(QW_ERR_IO, std::string("cannot open ") + path);
+    std::vector<uint8_t> bytes((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    return upload_packed(qwb::deserialize_layer(bytes), device, flags, out);
+  });
+}
+
 
 int qw_layer_free(qw_layer* L) {
   if (!L) return QW_OK;

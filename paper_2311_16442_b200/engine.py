@@ -195,6 +195,25 @@ class DeviceLayer:
         return {"codes2": codes2[:, :inf["n2_padded"]], "zeros2": zeros2[:, :gpr],
                 "scodes": scodes[:, :gpr], "codes4": codes4[:, :inf["n4"]]}
 
+    @classmethod
+    def load(cls, path, device: int = 0, kernel: str = "auto") -> "DeviceLayer":
+        """A QWL1 file (the reference's container, container.cpp:321-471)
+        straight to HBM (qw_layer_load): parse, CRC, validate, repack, copy."""
+        h = C.c_void_p()
+        flags = {"auto": 0, "mma": 1, "simt": 2}[kernel]
+        check(lib().qw_layer_load(str(path).encode(), device, flags, C.byref(h)))
+        out = cls(None, device, _handle=h, kernel=kernel)
+        return out
+
+    @classmethod
+    def from_qwl_bytes(cls, data: bytes, device: int = 0, kernel: str = "auto") -> "DeviceLayer":
+        """QWL1 bytes in memory (e.g. a memory-mapped cache) -> HBM."""
+        h = C.c_void_p()
+        buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
+        flags = {"auto": 0, "mma": 1, "simt": 2}[kernel]
+        check(lib().qw_layer_upload_qwl(buf, len(data), device, flags, C.byref(h)))
+        return cls(None, device, _handle=h, kernel=kernel)
+
     def clone(self) -> "DeviceLayer":
         """Device-to-device copy (distinct HBM buffers, same content)."""
         h = C.c_void_p()

@@ -69,6 +69,26 @@ def test_reference_written_layer_on_gpu(name, kernel):
 
 
 @pytest.mark.parametrize("name", GOLDEN_LAYERS)
+def test_reference_written_file_straight_to_device(name):
+    """qw_layer_load / qw_layer_upload_qwl: the
+    reference-written QWL1 file to HBM without a host PackedLayer; same
+    bit-exact K0/K1 and y as the host-object path."""
+    import torch
+    d = np.load(GOLD / f"layer_{name}.npz")
+    path = GOLD / f"layer_{name}.qwl"
+    for dl in (qw.DeviceLayer.load(path), qw.DeviceLayer.from_qwl_bytes(path.read_bytes(), kernel="mma")):
+        assert sha(dl.reconstruct_dense().cpu().numpy()) == str(d["recon_sha"])
+        un = {k: v.cpu().numpy() for k, v in dl.unpack().items()}
+        assert [sha(un[k]) for k in ("codes2", "zeros2", "scodes", "codes4")] == list(d["unpack_sha"])
+        check_y(dl.matvec(torch.from_numpy(d["x"]).cuda()).cpu().numpy(), d["y_f64"])
+    bad = bytearray(path.read_bytes())
+    bad[len(bad) // 2] ^= 0xFF  # the CRC32 catches it
+    with pytest.raises(qw.QWeightError) as ei:
+        qw.DeviceLayer.from_qwl_bytes(bytes(bad))
+    assert ei.value.status in (2, 8)
+
+
+@pytest.mark.parametrize("name", GOLDEN_LAYERS)
 def test_reference_written_layer_batched(name):
     """The same reference-written layers through the batched path (b = 4)."""
     import torch
