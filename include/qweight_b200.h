@@ -203,6 +203,13 @@ int qw_matvec_pdl(const qw_layer* layer, const float* x, uint32_t batch,
 #define QW_LAUNCH_X_INDEPENDENT 2u /* x was not written by the previous kernel
                                       on the stream: no dependency wait before
                                       reading it (q/k/v, gate/up share inputs) */
+/* Batched calls (batch >= 2): by default batch >= QW_GEMM_MIN_BATCH runs the
+ * tcgen05 GEMM K4 and smaller batches run the batch-1 kernel once per column
+ * (measured crossover: below 4 columns K4's fixed cost
+ * loses to per-column GEMVs).  These flags force one or the other. */
+#define QW_GEMM_MIN_BATCH 4u
+#define QW_LAUNCH_FORCE_GEMM 4u
+#define QW_LAUNCH_FORCE_COLUMNS 8u
 int qw_matvec_ex(const qw_layer* layer, const float* x, uint32_t batch, float* y,
                  qw_workspace* ws, void* stream, uint32_t flags);
 /* Group launch (batch 1): up to 4 layers that read the same activation
@@ -302,6 +309,7 @@ int qw_debug_gemm_timeline(const qw_layer* layer, const float* x, uint32_t batch
 
 /* Number of kernels one qw_matvec call launches. */
 int qw_launches_per_matvec(const qw_layer* layer, uint32_t batch);
+int qw_launches_per_matvec_ex(const qw_layer* layer, uint32_t batch, uint32_t flags);
 /* Diagnostics: the power of two P of the batched path's fp16 A tiles (each
  * element is RN_fp16(w * 2^-P), w the reconstruct_dense weight). */
 int qw_debug_gemm_shift(const qw_layer* layer, int* shift);

@@ -120,6 +120,7 @@ _SIGS = {
     "qw_debug_gemm_timeline": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
                                          C.c_void_p]),
     "qw_launches_per_matvec": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "qw_launches_per_matvec_ex": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32]),
     "qw_debug_gemm_shift": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     "qw_debug_knob": (C.c_uint32, [C.c_char_p, C.c_uint32]),
 }

@@ -332,6 +332,13 @@ int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
   return QW_OK;
 }
 
+// batched policy (qweight_b200.h): K4 from QW_GEMM_MIN_BATCH columns up
+bool uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
+  static const uint32_t min_batch = qwdev::knob("QW_GEMM_MIN_BATCH", QW_GEMM_MIN_BATCH);
+  if (batch < 2 || !L->dev.gemm.ok || (flags & QW_LAUNCH_FORCE_COLUMNS)) return false;
+  return (flags & QW_LAUNCH_FORCE_GEMM) || batch >= min_batch;
+}
+
 int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_workspace* ws,
                void* stream, bool pdl, uint32_t flags = 0) {
   if (int s = check_ws(L, ws, batch)) return s;
@@ -342,10 +349,9 @@ int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_w
     cudaError_t e = cudaSetDevice(L->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   }
-  static const bool no_gemm = qwdev::knob_str("QW_NO_GEMM") != nullptr;
   const uint32_t xflags = (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u;
   int e = 0;
-  if (batch >= 2 && L->dev.gemm.ok && !no_gemm) {
+  if (uses_gemm(L, batch, flags)) {
     e = qwdev::launch_gemm(L->dev, x, batch, y, stream);
   } else if (L->dev.mrecs) {
     const qwdev::DeviceLayer* one[1] = {&L->dev};
@@ -1036,7 +1042,11 @@ int qw_debug_gemm_shift(const qw_layer* L, int* shift) {
 }
 
 int qw_launches_per_matvec(const qw_layer* L, uint32_t batch) {
-  if (L && batch >= 2 && L->dev.gemm.ok && !qwdev::knob_str("QW_NO_GEMM")) return 2;  // x prologue (+ CSR), GEMM
+  return qw_launches_per_matvec_ex(L, batch, 0u);
+}
+
+int qw_launches_per_matvec_ex(const qw_layer* L, uint32_t batch, uint32_t flags) {
+  if (L && uses_gemm(L, batch, flags)) return 2;  // x prologue (+ CSR), GEMM
   return (int)batch;
 }
 

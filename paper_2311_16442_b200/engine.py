@@ -125,7 +125,7 @@ class DeviceLayer:
 
     # ---------------------------------------------------------------- forward
     def matvec(self, x, out=None, workspace: Workspace | None = None, stream=None,
-               pdl: bool = False, x_independent: bool = False):
+               pdl: bool = False, x_independent: bool = False, batched: str = "auto"):
         """y = W_q x on the GPU.  x: torch cuda fp32 [cols] or [batch, cols]
         in original channel order.  Returns fp32 [rows] / [batch, rows].
         pdl: programmatic dependent launch (weights stream under the previous
@@ -151,7 +151,9 @@ class DeviceLayer:
             raise QWeightError(1, "matvec: out must be a contiguous cuda float32 tensor of batch * rows "
                                   "elements on the activation's device")
         ws = workspace or default_workspace(self.device)
-        flags = (1 if pdl else 0) | (2 if x_independent else 0)
+        # batched: "auto" (K4 from 4 columns, per-column GEMVs below), "gemm"
+        # (force the tcgen05 GEMM K4), "columns" (force per-column GEMVs)
+        flags = (1 if pdl else 0) | (2 if x_independent else 0) | {"auto": 0, "gemm": 4, "columns": 8}[batched]
         check(lib().qw_matvec_ex(self._h, C.c_void_p(xb.data_ptr()), batch,
                                  C.c_void_p(out.data_ptr()), ws._h,
                                  C.c_void_p(_stream_handle(stream)), flags))
@@ -227,8 +229,8 @@ class DeviceLayer:
         weights (the following launch on the stream) into L2.  [] clears."""
         check(lib().qw_layer_set_prefetch(self._h, _handles(next_layers), len(next_layers)))
 
-    def launches_per_matvec(self, batch: int = 1) -> int:
-        return int(lib().qw_launches_per_matvec(self._h, batch))
+    def launches_per_matvec(self, batch: int = 1, batched: str = "auto") -> int:
+        return int(lib().qw_launches_per_matvec_ex(self._h, batch, {"auto": 0, "gemm": 4, "columns": 8}[batched]))
 
 
 class _ChainStep(C.Structure):
@@ -325,7 +327,9 @@ class LayerGroup:
         if outs is None:
             outs = [torch.empty(d.rows, dtype=torch.float32, device=x.device) for d in self.layers]
         ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
-        flags = (1 if pdl else 0) | (2 if x_independent else 0)
+        # batched: "auto" (K4 from 4 columns, per-column GEMVs below), "gemm"
+        # (force the tcgen05 GEMM K4), "columns" (force per-column GEMVs)
+        flags = (1 if pdl else 0) | (2 if x_independent else 0) | {"auto": 0, "gemm": 4, "columns": 8}[batched]
         check(lib().qw_group_matvec(self._h, C.c_void_p(x.data_ptr()), ptrs,
                                     C.c_void_p(_stream_handle(stream)), flags))
         return outs

@@ -1,6 +1,8 @@
-"""BASELINE config 3: Llama-2-7B shapes, batch 1/2/4/8/16 (K2 for b = 1, K4 for b >= 2).
-Per-call time from a CUDA-graph chain of N distinct layer copies (inputs > L2).
-usage: python scripts/batch_sweep.py [N] [nopdl]  -> one JSON line per (shape, batch)"""
+"""BASELINE config 3: Llama-2-7B shapes, batch 1/2/3/4/8/16: the batched
+policy (K4 from 4 columns, per-column batch-1 GEMVs below) against both
+forced paths (K4 tcgen05 GEMM; b x the batch-1 kernel).  Per-call time from a
+CUDA-graph chain of N distinct layer copies (inputs > L2).
+usage: python scripts/batch_sweep.py [N] [nopdl]  -> one JSON line per (shape, batch, path)"""
 import json
 import sys
 from pathlib import Path
@@ -19,13 +21,13 @@ for name, rows, cols in (("q_proj", 4096, 4096), ("gate_proj", 11008, 4096), ("d
     base = qw.DeviceLayer(layer)
     dls = [base] + [base.clone() for _ in range(N - 1)]
     payload = qw.payload_bytes(layer)
-    for b in (1, 2, 4, 8, 16):
+    for b, mode in [(1, "auto")] + [(b, m) for b in (2, 3, 4, 8, 16) for m in ("auto", "gemm", "columns")]:
         xs = torch.from_numpy(np.stack([qw.synth_activation(cols, 50 + i) for i in range(b)])).cuda()
         ys = torch.empty(N, b, rows, device="cuda")
 
         def run():
             for i, d in enumerate(dls):
-                d.matvec(xs, out=ys[i], pdl=PDL)
+                d.matvec(xs, out=ys[i], pdl=PDL, batched=mode)
         run()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -45,6 +47,7 @@ for name, rows, cols in (("q_proj", 4096, 4096), ("gate_proj", 11008, 4096), ("d
         balg = payload + 4 * b * (rows + cols)
         line = {"shape": name, "rows": rows, "cols": cols, "batch": b, "us_per_call": round(us, 3),
                 "gb_s": round(balg / us / 1e3, 1), "tflops": round(2 * b * rows * cols / us / 1e6, 2),
-                "path": "K2 fused GEMV" if b == 1 else "K4 tcgen05 GEMM",
-                "launches": base.launches_per_matvec(b)}
+                "mode": mode, "launches": base.launches_per_matvec(b, mode),
+                "path": "K4 tcgen05 GEMM" if (mode == "gemm" or (mode == "auto" and b >= 4)) else
+                        f"{b} x batch-1 {'K2m' if base.uses_tensor_core else 'K2'}"}
         print(json.dumps(line), flush=True)

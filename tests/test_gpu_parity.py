@@ -206,9 +206,10 @@ def test_batched_tensor_core_path(rows, cols, batch):
     torch = _torch()
     layer = qw.synth_layer(rows, cols, seed=rows + cols + batch, outlier_ratio=0.005)
     dl = qw.DeviceLayer(layer)
-    assert dl.launches_per_matvec(batch) == 2, "expected x prologue + tcgen05 GEMM"
+    assert dl.launches_per_matvec(batch, "gemm") == 2, "expected x prologue + tcgen05 GEMM"
+    assert dl.launches_per_matvec(batch) == (2 if batch >= 4 else batch)  # the default policy
     xs = np.stack([qw.synth_activation(cols, 300 + b) for b in range(batch)])
-    Y = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
+    Y = dl.matvec(torch.from_numpy(xs).cuda(), batched="gemm").cpu().numpy()
     assert np.all(np.isfinite(Y))
     for b in range(batch):
         ref = oracle.matvec_f64(layer, xs[b])
@@ -216,8 +217,12 @@ def test_batched_tensor_core_path(rows, cols, batch):
         assert err <= TOL, (b, err)
         assert np.max(np.abs(Y[b] - ref)) <= TOL * np.max(np.abs(ref))
     # deterministic run to run (fixed split-K summation order)
-    Y2 = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
+    Y2 = dl.matvec(torch.from_numpy(xs).cuda(), batched="gemm").cpu().numpy()
     assert np.array_equal(Y, Y2)
+    # the per-column path agrees within the tolerance
+    Yc = dl.matvec(torch.from_numpy(xs).cuda(), batched="columns").cpu().numpy()
+    for b in range(batch):
+        assert rel_l2(Yc[b], oracle.matvec_f64(layer, xs[b])) <= TOL
 
 
 def test_batched_unsupported_geometry_falls_back_to_columns():
@@ -225,7 +230,7 @@ def test_batched_unsupported_geometry_falls_back_to_columns():
     torch = _torch()
     layer = qw.synth_layer(24, 160, seed=4, alpha=0.5)
     dl = qw.DeviceLayer(layer)
-    assert dl.launches_per_matvec(3) == 3
+    assert dl.launches_per_matvec(3, "gemm") == 3
     xs = np.stack([qw.synth_activation(160, 40 + b) for b in range(3)])
     Y = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
     for b in range(3):
