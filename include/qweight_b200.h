@@ -203,10 +203,11 @@ int qw_matvec_pdl(const qw_layer* layer, const float* x, uint32_t batch,
 #define QW_LAUNCH_X_INDEPENDENT 2u /* x was not written by the previous kernel
                                       on the stream: no dependency wait before
                                       reading it (q/k/v, gate/up share inputs) */
-/* Batched calls (batch >= 2): by default batch >= QW_GEMM_MIN_BATCH runs the
- * tcgen05 GEMM K4 and smaller batches run the batch-1 kernel once per column
- * (measured crossover: below 4 columns K4's fixed cost
- * loses to per-column GEMVs).  These flags force one or the other. */
+/* Batched calls (batch >= 2): by default batch >= QW_GEMM_MIN_BATCH (3 for a
+ * layer of at most 4096 x 4096 weights) runs the tcgen05 GEMM K4 and smaller
+ * batches run the batch-1 kernel once per column (the measured crossover,
+ * profiles/r02_batch_sweep.jsonl: below it K4's fixed cost loses to
+ * per-column GEMVs).  These flags force one or the other. */
 #define QW_GEMM_MIN_BATCH 4u
 #define QW_LAUNCH_FORCE_GEMM 4u
 #define QW_LAUNCH_FORCE_COLUMNS 8u

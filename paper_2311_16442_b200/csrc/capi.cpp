@@ -332,10 +332,14 @@ int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
   return QW_OK;
 }
 
-// batched policy (qweight_b200.h): K4 from QW_GEMM_MIN_BATCH columns up
+// batched policy (qweight_b200.h): K4 from QW_GEMM_MIN_BATCH columns up; a
+// layer of at most 4096 x 4096 weights from 3 (its per-column GEMV is cheap
+// against K4's fixed cost only up to 2 columns: profiles/r02_batch_sweep.jsonl)
 bool uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
-  static const uint32_t min_batch = qwdev::knob("QW_GEMM_MIN_BATCH", QW_GEMM_MIN_BATCH);
+  static const uint32_t forced = qwdev::knob("QW_GEMM_MIN_BATCH", 0);
   if (batch < 2 || !L->dev.gemm.ok || (flags & QW_LAUNCH_FORCE_COLUMNS)) return false;
+  const uint64_t weights = (uint64_t)L->dev.g.rows * L->dev.g.cols;
+  const uint32_t min_batch = forced ? forced : (weights <= 4096ull * 4096ull ? 3u : QW_GEMM_MIN_BATCH);
   return (flags & QW_LAUNCH_FORCE_GEMM) || batch >= min_batch;
 }
 

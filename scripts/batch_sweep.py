@@ -48,6 +48,6 @@ for name, rows, cols in (("q_proj", 4096, 4096), ("gate_proj", 11008, 4096), ("d
         line = {"shape": name, "rows": rows, "cols": cols, "batch": b, "us_per_call": round(us, 3),
                 "gb_s": round(balg / us / 1e3, 1), "tflops": round(2 * b * rows * cols / us / 1e6, 2),
                 "mode": mode, "launches": base.launches_per_matvec(b, mode),
-                "path": "K4 tcgen05 GEMM" if (mode == "gemm" or (mode == "auto" and b >= 4)) else
+                "path": "K4 tcgen05 GEMM" if (mode == "gemm" or (mode == "auto" and b >= (3 if rows * cols <= 4096 ** 2 else 4))) else
                         f"{b} x batch-1 {'K2m' if base.uses_tensor_core else 'K2'}"}
         print(json.dumps(line), flush=True)
