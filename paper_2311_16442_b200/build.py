@@ -16,6 +16,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libqweight_b200.so"
+TP_LIB = LIB_DIR / "libqweight_b200_tp.so"  # the NCCL tensor-parallel entries (qweight_b200_tp.h)
 OBJ_DIR = PKG / "lib" / "obj"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -39,9 +40,9 @@ def _cuda_home() -> Path:
 
 def _sources():
     host = sorted((CSRC / "host").glob("*.cpp")) + [CSRC / "capi.cpp"]
-    dev = sorted((CSRC / "device").glob("*.cu"))
+    dev = sorted((CSRC / "device").glob("*.cu"))  # (csrc/tp/ builds the separate TP library)
     headers = (sorted(CSRC.rglob("*.hpp")) + sorted(CSRC.rglob("*.cuh")) + sorted(CSRC.rglob("*.inl")) +
-               [ROOT / "include" / "qweight_b200.h"])
+               [ROOT / "include" / "qweight_b200.h", ROOT / "include" / "qweight_b200_tp.h"])
     return host, dev, headers
 
 
@@ -85,6 +86,12 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         if force or _stale(LIB, objs):
             _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB),
                   *map(str, objs), "-lpthread"], log)
+        # the TP library: depends on the main library and NCCL (libnccl.so.2)
+        tp_src = sorted((CSRC / "tp").glob("*.cu"))
+        if tp_src and (force or _stale(TP_LIB, [*tp_src, LIB, *headers])):
+            _run([nvcc, *NVCCFLAGS, f"-I{ROOT / 'include'}", "-shared", "-cudart", "shared", "-o", str(TP_LIB),
+                  *map(str, tp_src), f"-L{LIB_DIR}", "-lqweight_b200", "-lnccl",
+                  "-Xlinker", "-rpath,$ORIGIN"], log)
     return LIB
 
 
