@@ -100,3 +100,15 @@ def test_diagnostic_knobs_are_inert_without_the_debug_gate():
                                    text=True, check=True).stdout.split()
     assert run(env) == ["2", "0", "4"]          # defaults pinned
     assert run({**env, "QW_DEBUG_KNOBS": "1"}) == ["1", "3", "9"]  # the gate opens them
+
+
+def test_tp_library_exports_its_header():
+    """include/qweight_b200_tp.h <-> libqweight_b200_tp.so (NCCL entries)."""
+    tp_h = ROOT / "include" / "qweight_b200_tp.h"
+    text = re.sub(r"/\*.*?\*/", "", tp_h.read_text(), flags=re.S)
+    declared = set(re.findall(r"\b(qw_tp_[a-z0-9_]+)\s*\(", text))
+    assert declared == {"qw_tp_create", "qw_tp_matvec", "qw_tp_local_extent", "qw_tp_free"}
+    lib = _native.lib_path().parent / "libqweight_b200_tp.so"
+    out = subprocess.run(["nm", "-D", "--defined-only", str(lib)], capture_output=True, text=True, check=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert declared <= exported
