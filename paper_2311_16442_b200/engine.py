@@ -327,9 +327,7 @@ class LayerGroup:
         if outs is None:
             outs = [torch.empty(d.rows, dtype=torch.float32, device=x.device) for d in self.layers]
         ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
-        # batched: "auto" (K4 from 4 columns, per-column GEMVs below), "gemm"
-        # (force the tcgen05 GEMM K4), "columns" (force per-column GEMVs)
-        flags = (1 if pdl else 0) | (2 if x_independent else 0) | {"auto": 0, "gemm": 4, "columns": 8}[batched]
+        flags = (1 if pdl else 0) | (2 if x_independent else 0)
         check(lib().qw_group_matvec(self._h, C.c_void_p(x.data_ptr()), ptrs,
                                     C.c_void_p(_stream_handle(stream)), flags))
         return outs
