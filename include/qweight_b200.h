@@ -112,6 +112,13 @@ int qw_host_quantize(const float* w, uint32_t rows, uint32_t cols,
                      double outlier_ratio, uint32_t threads,
                      qw_host_layer** out);
 /* Copy + validate_layer a borrowed view into an owning host layer. */
+/* quantize_layer with its data-parallel passes on the GPU (channel
+ * amplitudes, outlier scores + top-K candidates, group fits, the 2-order
+ * pass): the same host layer as qw_host_quantize, bit for
+ * bit (the plan ranking, final top-K order, CSR and pack stay on the host). */
+int qw_device_quantize(const float* w, uint32_t rows, uint32_t cols, const float* h,
+                       double alpha, uint32_t group2, double ratio, int device,
+                       qw_host_layer** out);
 int qw_host_from_view(const qw_layer_view* view, qw_host_layer** out);
 /* Borrowed view of an owning host layer (valid until qw_host_free). */
 int qw_host_view(const qw_host_layer* layer, qw_layer_view* view);

@@ -5,13 +5,13 @@ fp16 sparse outliers, behind the reference's host API.
 """
 from ._native import QWeightError, exported_symbols, lib
 from .layer import (PAD, LayerConfig, PackedLayer, payload_bytes, permute, plant_outliers,
-                    quantize_layer, read_packed_layer, shard_rows, shard_tiles,
+                    quantize_layer, quantize_layer_gpu, read_packed_layer, shard_rows, shard_tiles,
                     synth_activation, synth_calibration, synth_gaussian, synth_layer,
                     validate_layer, write_packed_layer)
 
 __all__ = [
     "QWeightError", "LayerConfig", "PackedLayer", "PAD", "lib", "exported_symbols",
-    "payload_bytes", "permute", "plant_outliers", "quantize_layer", "read_packed_layer",
+    "payload_bytes", "permute", "plant_outliers", "quantize_layer", "quantize_layer_gpu", "read_packed_layer",
     "shard_rows", "shard_tiles", "synth_activation", "synth_calibration", "synth_gaussian",
     "synth_layer", "validate_layer", "write_packed_layer", "DeviceLayer", "Workspace",
     "MatvecResult", "upload", "LayerGroup", "DecodeChain",

@@ -64,6 +64,8 @@ _SIGS = {
     "qw_last_error": (C.c_char_p, []),
     "qw_host_quantize": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_double,
                                    C.c_uint32, C.c_double, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "qw_device_quantize": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_double, C.c_uint32,
+                                     C.c_double, C.c_int, C.POINTER(C.c_void_p)]),
     "qw_host_from_view": (C.c_int, [C.POINTER(LayerView), C.POINTER(C.c_void_p)]),
     "qw_host_view": (C.c_int, [C.c_void_p, C.POINTER(LayerView)]),
     "qw_host_free": (None, [C.c_void_p]),

@@ -487,6 +487,24 @@ int qw_host_quantize(const float* w, uint32_t rows, uint32_t cols, const float* 
   });
 }
 
+int qw_device_quantize(const float* w, uint32_t rows, uint32_t cols, const float* h, double alpha,
+                       uint32_t group2, double ratio, int device, qw_host_layer** out) {
+  return guarded([&] {
+    if (!w || !h || !out) return fail(QW_ERR_ARG, "quantize: null argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      return fail(QW_ERR_CUDA, "device quantize: no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(QW_ERR_ARG, "device quantize: device index out of range");
+    qwb::QuantizeParams p;
+    p.alpha = alpha, p.group2 = group2, p.outlier_ratio = ratio;
+    auto H = std::make_unique<qw_host_layer>();
+    H->L = qwb::quantize_layer_gpu(w, rows, cols, {h, cols}, p, device);
+    H->refresh_soa();
+    *out = H.release();
+    return (int)QW_OK;
+  });
+}
+
 int qw_host_from_view(const qw_layer_view* v, qw_host_layer** out) {
   return guarded([&] {
     if (!v || !out) return fail(QW_ERR_ARG, "from_view: null argument");

@@ -146,6 +146,11 @@ std::vector<float> synth_activation(uint32_t cols, uint64_t seed);
 
 ChannelPlan build_plan_from(const WeightMatrix& w, std::span<const float> h,
                             double alpha, unsigned threads);
+ChannelPlan plan_from_amplitudes(const std::vector<double>& amp, uint32_t ic, double alpha);
+// quantize_layer with its data-parallel passes on the GPU (qwb_gpu_producer.cpp,
+// qw_quantize.cu): bit-identical to quantize_layer.
+PackedLayer quantize_layer_gpu(const float* w, uint32_t rows, uint32_t cols, std::span<const float> h,
+                               const QuantizeParams& p, int device);
 PackedLayer quantize_layer(const WeightMatrix& w, std::span<const float> h,
                            const QuantizeParams& p, unsigned threads);
 PackedLayer pack_layer(const LayerConfig& cfg, const ChannelPlan& plan,

@@ -98,6 +98,12 @@ ChannelPlan build_plan_from(const WeightMatrix& w, std::span<const float> h,
     }
   });
 
+  return plan_from_amplitudes(amp, ic, alpha);
+}
+
+// build_plan (plan.cpp:32-73) from the channel amplitudes: the top n4 by
+// (amplitude desc, index asc) become 4-bit; layout [2-bit asc | pads | 4-bit asc].
+ChannelPlan plan_from_amplitudes(const std::vector<double>& amp, uint32_t ic, double alpha) {
   uint32_t n4 = 16u * (uint32_t)std::floor(alpha * (double)ic / 16.0 + 0.5);
   n4 = std::min(n4, ic);
   std::vector<uint32_t> idx(ic);

@@ -214,6 +214,18 @@ def quantize_layer(w: np.ndarray, h: np.ndarray, alpha: float = 0.25, group2: in
     return PackedLayer._from_handle(hd)
 
 
+def quantize_layer_gpu(w: np.ndarray, h: np.ndarray, alpha: float = 0.25, group2: int = 16,
+                       outlier_ratio: float = 0.002, device: int = 0) -> PackedLayer:
+    """quantize_layer with its data-parallel passes on the GPU (qw_device_quantize):
+    the same PackedLayer as quantize_layer, bit for bit."""
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    h = np.ascontiguousarray(h, dtype=np.float32)
+    out = C.c_void_p()
+    check(lib().qw_device_quantize(w.ctypes.data, w.shape[0], w.shape[1], h.ctypes.data, alpha, group2,
+                                   outlier_ratio, device, C.byref(out)))
+    return PackedLayer._from_handle(out)
+
+
 def synth_layer(rows: int, cols: int, seed: int = 7, alpha: float = 0.25, group2: int = 16,
                 outlier_ratio: float = 0.002, threads: int = 0) -> PackedLayer:
     """The benchmark recipe: W = synth_gaussian(seed), H = synth_calibration(seed)."""
