@@ -210,12 +210,14 @@ int qw_matvec_pdl(const qw_layer* layer, const float* x, uint32_t batch,
 #define QW_LAUNCH_X_INDEPENDENT 2u /* x was not written by the previous kernel
                                       on the stream: no dependency wait before
                                       reading it (q/k/v, gate/up share inputs) */
-/* Batched calls (batch >= 2): by default batch >= QW_GEMM_MIN_BATCH (3 for a
- * layer of at most 4096 x 4096 weights) runs the tcgen05 GEMM K4 and smaller
- * batches run the batch-1 kernel once per column (the measured crossover,
- * profiles/r02_batch_sweep.jsonl: below it K4's fixed cost loses to
- * per-column GEMVs).  These flags force one or the other. */
-#define QW_GEMM_MIN_BATCH 4u
+/* Batched calls (batch >= 2): by default batch >= QW_GEMM_MIN_BATCH runs the
+ * tcgen05 GEMM K4; smaller batches run the batch-1 kernel over the columns,
+ * up to 4 columns sharing one launch (the grid split over the columns, each
+ * column's result bit-identical to its own batch-1 call; the weights are
+ * read from HBM about once and shared through L2).  The crossover is
+ * measured (profiles/r02_batch_sweep_*.jsonl).  These flags force one or the
+ * other. */
+#define QW_GEMM_MIN_BATCH 5u
 #define QW_LAUNCH_FORCE_GEMM 4u
 #define QW_LAUNCH_FORCE_COLUMNS 8u
 int qw_matvec_ex(const qw_layer* layer, const float* x, uint32_t batch, float* y,
@@ -318,6 +320,9 @@ int qw_debug_gemm_timeline(const qw_layer* layer, const float* x, uint32_t batch
 /* Number of kernels one qw_matvec call launches. */
 int qw_launches_per_matvec(const qw_layer* layer, uint32_t batch);
 int qw_launches_per_matvec_ex(const qw_layer* layer, uint32_t batch, uint32_t flags);
+/* 1 if a qw_matvec_ex call of `batch` columns with `flags` runs the tcgen05
+ * GEMM K4, 0 if it runs the batch-1 kernel over the columns; < 0 on error. */
+int qw_matvec_uses_gemm(const qw_layer* layer, uint32_t batch, uint32_t flags);
 /* Diagnostics: the power of two P of the batched path's fp16 A tiles (each
  * element is RN_fp16(w * 2^-P), w the reconstruct_dense weight). */
 int qw_debug_gemm_shift(const qw_layer* layer, int* shift);

@@ -123,6 +123,7 @@ _SIGS = {
                                          C.c_void_p]),
     "qw_launches_per_matvec": (C.c_int, [C.c_void_p, C.c_uint32]),
     "qw_launches_per_matvec_ex": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32]),
+    "qw_matvec_uses_gemm": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32]),
     "qw_debug_gemm_shift": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     "qw_debug_knob": (C.c_uint32, [C.c_char_p, C.c_uint32]),
 }

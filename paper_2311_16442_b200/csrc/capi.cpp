@@ -314,10 +314,11 @@ void free_dev(qwdev::DeviceLayer& d) {
 cudaError_t alloc_mma_scratch(qwdev::DeviceLayer& d) {
   const auto& m = d.mg;
   cudaError_t e = cudaSuccess;
-  if (m.nchunks > 1) {
-    if ((e = cudaMalloc((void**)&d.mpart, (size_t)(m.nchunks + 1) * m.RT * 16 * 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc((void**)&d.mcnt, (size_t)m.RT * 4)) != cudaSuccess) return e;
-    e = cudaMemset(d.mcnt, 0, (size_t)m.RT * 4);
+  if (m.nchunks > 1) {  // one slot per column of a column launch (launch_columns)
+    const size_t slots = qwdev::kMaxSeg;
+    if ((e = cudaMalloc((void**)&d.mpart, slots * (m.nchunks + 1) * m.RT * 16 * 4)) != cudaSuccess) return e;
+    if ((e = cudaMalloc((void**)&d.mcnt, slots * m.RT * 4)) != cudaSuccess) return e;
+    e = cudaMemset(d.mcnt, 0, slots * m.RT * 4);
   }
   return e;
 }
@@ -332,15 +333,22 @@ int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
   return QW_OK;
 }
 
-// batched policy (qweight_b200.h): K4 from QW_GEMM_MIN_BATCH columns up; a
-// layer of at most 4096 x 4096 weights from 3 (its per-column GEMV is cheap
-// against K4's fixed cost only up to 2 columns: profiles/r02_batch_sweep.jsonl)
+// batched policy (qweight_b200.h): K4 from QW_GEMM_MIN_BATCH columns up, the
+// batch-1 kernel over the columns (4 to a launch) below -- at 2..4 columns
+// one column launch beats K4's fixed cost on every 7B shape
+// (profiles/r02_batch_sweep_simt.jsonl)
 bool uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
   static const uint32_t forced = qwdev::knob("QW_GEMM_MIN_BATCH", 0);
   if (batch < 2 || !L->dev.gemm.ok || (flags & QW_LAUNCH_FORCE_COLUMNS)) return false;
-  const uint64_t weights = (uint64_t)L->dev.g.rows * L->dev.g.cols;
-  const uint32_t min_batch = forced ? forced : (weights <= 4096ull * 4096ull ? 3u : QW_GEMM_MIN_BATCH);
+  const uint32_t min_batch = forced ? forced : QW_GEMM_MIN_BATCH;
   return (flags & QW_LAUNCH_FORCE_GEMM) || batch >= min_batch;
+}
+
+// columns of a batch share launches (qw_columns.cu); QW_COLUMN_GROUP=0 (debug
+// knob) runs one launch per column for A/B measurements
+bool column_groups() {
+  static const uint32_t on = qwdev::knob("QW_COLUMN_GROUP", 1);
+  return on != 0;
 }
 
 int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_workspace* ws,
@@ -357,6 +365,8 @@ int run_matvec(const qw_layer* L, const float* x, uint32_t batch, float* y, qw_w
   int e = 0;
   if (uses_gemm(L, batch, flags)) {
     e = qwdev::launch_gemm(L->dev, x, batch, y, stream);
+  } else if (batch > 1 && column_groups()) {
+    e = qwdev::launch_columns(L->dev, x, batch, y, stream, pdl, xflags);
   } else if (L->dev.mrecs) {
     const qwdev::DeviceLayer* one[1] = {&L->dev};
     for (uint32_t col = 0; col < batch && !e; ++col) {
@@ -442,6 +452,7 @@ int upload_packed(const qwb::PackedLayer& L, int device, uint32_t flags, qw_laye
         return cuda_fail((cudaError_t)pe, "mma plan");
       }
     }
+    qwdev::plan_columns(H->dev, H->num_sms, H->host_row_ptr.data());
     *out = H.release();
     return (int)QW_OK;
   }
@@ -866,6 +877,7 @@ int qw_layer_clone(const qw_layer* L, qw_layer** out) {
       return cuda_fail((cudaError_t)pe, "mma plan");
     }
   }
+  qwdev::plan_columns(H->dev, H->num_sms, H->host_row_ptr.data());
   *out = H.release();
   return QW_OK;
 }
@@ -1037,7 +1049,8 @@ int qw_debug_group_timeline(const qw_group* g, const float* x, float* const* ys,
                             uint32_t flags, void* stream) {
   if (!g || !x || !ys || !stamps) return fail(QW_ERR_ARG, "timeline: null argument");
   cudaSetDevice(g->device);
-  const int e = qwdev::launch_gemv_group(g->plan, g->layers.data(), (uint32_t)g->layers.size(), x, ys, stream,
+  const float* xs[qwdev::kMaxSeg] = {x, x, x, x};
+  const int e = qwdev::launch_gemv_group(g->plan, g->layers.data(), (uint32_t)g->layers.size(), xs, ys, stream,
                                          flags & 1u, (flags & 4u) ? qwdev::kXIndependent : 0u, stamps, 1,
                                          (flags & 2u) != 0);
   return e ? cuda_fail((cudaError_t)e, "group launch") : QW_OK;
@@ -1067,8 +1080,14 @@ int qw_launches_per_matvec(const qw_layer* L, uint32_t batch) {
   return qw_launches_per_matvec_ex(L, batch, 0u);
 }
 
+int qw_matvec_uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
+  if (!L) return fail(QW_ERR_ARG, "uses_gemm: null layer");
+  return uses_gemm(L, batch, flags) ? 1 : 0;
+}
+
 int qw_launches_per_matvec_ex(const qw_layer* L, uint32_t batch, uint32_t flags) {
   if (L && uses_gemm(L, batch, flags)) return 2;  // x prologue (+ CSR), GEMM
+  if (L && batch > 1 && column_groups()) return (int)qwdev::column_launches(L->dev, batch);
   return (int)batch;
 }
 

@@ -118,7 +118,11 @@ struct GemmPlan {
 //                codes 32 lanes x 4 u32 (E_g, E_g+8, O_g, O_g+8)
 //   4-bit block: codes 32 lanes x 8 u32, s4 32 lanes x 2 u32, z4 32 lanes x u16
 // Lane (g, t) of a block owns rows {g, g+8} and columns {2t, 2t+1}.
-constexpr uint32_t kMmaMaxChunks = 8, kMmaMaxBlk = 32;
+#ifndef QW_MMA_NW
+#define QW_MMA_NW 16
+#endif
+constexpr uint32_t kMmaMaxChunks = 16, kMmaMaxBlk = 32;
+constexpr uint32_t kMmaChunkBlk = 2 * QW_MMA_NW;  // blocks per chunk: consumer warps x 2
 constexpr uint32_t kMmaHdr2 = 352, kMmaCode2 = 512, kMmaCode4 = 1024, kMmaS4 = 256, kMmaZ4 = 64;
 struct MmaChunk {
   uint32_t nblk = 0, rec_bytes = 0;
@@ -145,9 +149,11 @@ struct DeviceLayer {
   GemmPlan gemm;
   MmaGeometry mg;
   MmaPlan mplan;
+  GemvPlan cplan[kMaxSeg - 1];    // column launches of 2..kMaxSeg columns (grid 0: not planned)
+  MmaPlan mcplan[kMaxSeg - 1];
   uint8_t* mrecs = nullptr;       // RT x nchunks records (chunk-major), rec_stride apart
-  float* mpart = nullptr;         // [nchunks][RT*16] chunk partial sums, then [RT*16] CSR sums
-  uint32_t* mcnt = nullptr;       // [RT] chunk arrivals (self-resetting)
+  float* mpart = nullptr;         // per column slot (kMaxSeg): [nchunks][RT*16] chunk partials, [RT*16] CSR sums
+  uint32_t* mcnt = nullptr;       // per column slot: [RT] chunk arrivals (self-resetting)
   uint8_t* quads = nullptr;      // quads * dense_bytes
   uint32_t* sorder = nullptr;    // row_blocks * G2s
   uint32_t* perm = nullptr;      // padded_cols (0xFFFFFFFF = pad)
@@ -176,9 +182,17 @@ int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_
                     uint32_t n, int num_sms);
 int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
                       float* const* ys, void* stream, bool pdl, uint32_t flags);
-int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
+int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
                       float* const* ys, void* stream, bool pdl, uint32_t flags, unsigned long long* dbg,
                       uint32_t repeat, bool global_clock);
+// Batch of 2..16 columns on the batch-1 kernel of the layer (K2 or K2m): the
+// columns go kMaxSeg to a launch, one grid split over them like a layer
+// group (each segment its own x and y, the same weights, read once from HBM
+// and shared through L2).  Plans: plan_columns at upload (cplan / mcplan).
+int plan_columns(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr);
+int launch_columns(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream, bool pdl,
+                   uint32_t flags);
+uint32_t column_launches(const DeviceLayer& L, uint32_t batch);
 // y[col] = W_q x[col] for col < batch: one fused kernel per column.
 constexpr uint32_t kTimelineEvents = 12;  // entry, copies issued, prologue, first quad, consumers, y, csr
 // flags: kXIndependent = x was not written by the preceding kernel on the
@@ -204,6 +218,9 @@ int plan_mma(MmaPlan& p, const DeviceLayer* const* layers, const uint32_t* const
              int num_sms);
 int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
                float* const* ys, void* stream, bool pdl, uint32_t flags);
+// segment s reads xs[s]; column_slots: segment s uses the layer's scratch slot s
+int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
+               float* const* ys, void* stream, bool pdl, uint32_t flags, bool column_slots);
 
 // Decode chain (batch 1): a sequence of launch steps (each a group of 1..4
 // layers of identical geometry reading one activation) run by ONE persistent

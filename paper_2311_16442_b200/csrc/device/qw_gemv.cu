@@ -65,7 +65,7 @@ struct GemvArgs {
   float* y[kMaxSeg];
   float s_scale[kMaxSeg];  // 2^-P: keeps (eff - zero2) scale2 2^-P inside fp16
   uint32_t seg_rows[kMaxSeg];  // output rows of each layer (a group may mix row counts: GQA q/k/v)
-  const float* x;
+  const float* xs[kMaxSeg];    // the segment's input: one x for a layer group, one column each for a batch
   Geometry g;
   uint32_t W, W2, T, S, grid, nq_max;  // warps per team, 2-bit warps, teams, ring slots
   uint32_t rb_magic, rb_one;  // row / group2 = rb_one ? row : umulhi(row, rb_magic)
@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
   const uint32_t* __restrict__ g_csr = a.csr[seg];
   const uint16_t* __restrict__ g_perm = a.perm[seg];
   float* __restrict__ g_y = a.y[seg];
+  const float* __restrict__ g_x = a.xs[seg];
   const float s_scale = a.s_scale[seg];
   const uint32_t nunit = (nq + NQ - 1) / NQ;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
@@ -245,13 +246,13 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
           for (int j = 0; j < 4; ++j) w[j] = s_ent[e + j];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const float xv = XSM ? s_x[w[j] & 0xFFFFu] : __ldg(a.x + (w[j] & 0xFFFFu));
+            const float xv = XSM ? s_x[w[j] & 0xFFFFu] : __ldg(g_x + (w[j] & 0xFFFFu));
             acc = __fadd_rn(acc, __fmul_rn(half_bits_to_float(w[j] >> 16), xv));  // no contraction
           }
         }
         for (; e < hi; ++e) {
           const uint32_t w = s_ent[e];
-          acc = __fadd_rn(acc, __fmul_rn(half_bits_to_float(w >> 16), XSM ? s_x[w & 0xFFFFu] : __ldg(a.x + (w & 0xFFFFu))));
+          acc = __fadd_rn(acc, __fmul_rn(half_bits_to_float(w >> 16), XSM ? s_x[w & 0xFFFFu] : __ldg(g_x + (w & 0xFFFFu))));
         }
         s_csr[t] = acc;
       }
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
         const uint32_t e = c0 + lane + 32u * j;
-        if (e < c1) s_prod[e - c0] = half_bits_to_float(ent[j] >> 16) * (XSM ? s_x[src[j]] : __ldg(a.x + src[j]));
+        if (e < c1) s_prod[e - c0] = half_bits_to_float(ent[j] >> 16) * (XSM ? s_x[src[j]] : __ldg(g_x + src[j]));
       }
       __syncwarp();
       if (c1 < n) fetch(c1);
@@ -414,8 +415,8 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     // co-reside with it): the loads are issued first and land under the
     // scale decode below; else after it (the decode overlaps the predecessor).
     const uint32_t tid = threadIdx.x, nth = NC * 32u;
-    const bool xvec = (((uintptr_t)a.x) & 15u) == 0 && (G.cols & 3u) == 0;
-    const float4* gx = reinterpret_cast<const float4*>(a.x);
+    const bool xvec = (((uintptr_t)g_x) & 15u) == 0 && (G.cols & 3u) == 0;
+    const float4* gx = reinterpret_cast<const float4*>(g_x);
     float4* sx4 = reinterpret_cast<float4*>(s_x);
     const uint32_t n4 = G.cols >> 2;
     constexpr int kXr = 4;
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
             if (i + j * nth < n4) sx4[i + j * nth] = v[j];
         }
       } else {
-        for (uint32_t i = tid; i < G.cols; i += nth) s_x[i] = __ldg(a.x + i);
+        for (uint32_t i = tid; i < G.cols; i += nth) s_x[i] = __ldg(g_x + i);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(s_xbar);
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
       xs = s_x;
     } else {
       if (a.wait_x) pdl_wait();  // x is the previous kernel's output
-      xs = a.x;
+      xs = g_x;
     }
     // Two teams need the same X: team 0 prepares it and hands it to team 1
     // through team 1's (not yet used) reduction windows.
@@ -952,7 +953,7 @@ int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_
   return plan_ctas(p, G, host_row_ptrs, rows, n, num_sms);
 }
 
-int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
+int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
                       float* const* ys, void* stream, bool pdl, uint32_t flags, unsigned long long* dbg,
                       uint32_t repeat, bool global_clock) {
   const Geometry& G = layers[0]->g;
@@ -962,9 +963,9 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
     a.quads[l] = L.quads, a.sorder[l] = L.sorder, a.row_ptr[l] = L.row_ptr;
     a.csr[l] = L.csr, a.perm[l] = L.perm16, a.s_scale[l] = L.plan.s_scale;
     a.y[l] = ys[std::min(l, n - 1)];
+    a.xs[l] = xs[std::min(l, n - 1)];
     a.seg_rows[l] = L.g.rows;
   }
-  a.x = x;
   a.g = G;
   a.W = p.warps, a.W2 = p.warps2, a.T = p.teams, a.S = p.nslot;
   a.grid = p.grid, a.nq_max = p.nq_max, a.rb_magic = p.rb_magic, a.rb_one = p.rb_one;
@@ -992,7 +993,8 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
 
 int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
                       float* const* ys, void* stream, bool pdl, uint32_t flags) {
-  return launch_gemv_group(p, layers, n, x, ys, stream, pdl, flags, nullptr, 1, false);
+  const float* xs[kMaxSeg] = {x, x, x, x};
+  return launch_gemv_group(p, layers, n, xs, ys, stream, pdl, flags, nullptr, 1, false);
 }
 
 int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream,
@@ -1001,8 +1003,8 @@ int launch_gemv(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   const DeviceLayer* layers[1] = {&L};
   for (uint32_t col = 0; col < batch; ++col) {
     float* ys[1] = {y + (size_t)col * L.g.rows};
-    const int e = launch_gemv_group(L.plan, layers, 1, x + (size_t)col * L.g.cols, ys, stream, pdl, flags,
-                                    dbg, repeat, global_clock);
+    const float* xs[1] = {x + (size_t)col * L.g.cols};
+    const int e = launch_gemv_group(L.plan, layers, 1, xs, ys, stream, pdl, flags, dbg, repeat, global_clock);
     if (e) return e;
   }
   return 0;

@@ -59,11 +59,11 @@ void mma_geometry(MmaGeometry& m, const Geometry& g) {
   // chunks of at most 32 blocks, each an even share of the 2-bit and of the
   // 4-bit blocks (records of similar size and work)
   auto span = [](uint32_t n, uint32_t c, uint32_t k) { return (c + 1) * n / k - c * n / k; };
-  uint32_t nc = (nb + kMmaMaxBlk - 1) / kMmaMaxBlk;
+  uint32_t nc = (nb + kMmaChunkBlk - 1) / kMmaChunkBlk;
   for (;; ++nc) {
     uint32_t mx = 0;
     for (uint32_t c = 0; c < nc; ++c) mx = std::max(mx, span(nb2, c, nc) + span(nb4, c, nc));
-    if (mx <= kMmaMaxBlk) break;
+    if (mx <= kMmaChunkBlk) break;
   }
   if (nc > kMmaMaxChunks) return;
   m.nchunks = nc;
@@ -101,7 +101,7 @@ void mma_geometry(MmaGeometry& m, const Geometry& g) {
 
 namespace {
 
-constexpr uint32_t kNW = 16;                    // consumer warps
+constexpr uint32_t kNW = QW_MMA_NW;             // consumer warps
 constexpr uint32_t kThreads = (kNW + 2) * 32;   // + producer + CSR warp
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -331,7 +331,7 @@ struct MmaArgs {
   uint32_t* cnt[kMaxSeg];
   uint32_t rows[kMaxSeg], RT[kMaxSeg];
   float inv_s_scale[kMaxSeg];
-  const float* x;
+  const float* xs[kMaxSeg];
   uint32_t cols, n2p, G2, T4, nchunks, wait_x;
   MmaLayout lay;
   MmaChunk chunk[kMmaMaxChunks];
@@ -717,14 +717,14 @@ __device__ __forceinline__ void init_barriers(uint64_t* bars, uint32_t S) {
   if (threadIdx.x >= 64 && threadIdx.x < 68) mbar_init(&bars[2 * S + 1 + (threadIdx.x - 64)], 1);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) mma_gemv_kernel(const __grid_constant__ MmaArgs a) {
+__global__ void __launch_bounds__(kThreads, kNW <= 8 ? 2 : 1) mma_gemv_kernel(const __grid_constant__ MmaArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
   const MmaLayout& L = a.lay;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t seg = a.cta_seg[blockIdx.x];
   StepView v{a.recs[seg], a.perm16[seg], a.row_ptr[seg], a.csr[seg], a.y[seg], a.part[seg], a.cnt[seg],
-             a.rows[seg], a.RT[seg], a.inv_s_scale[seg], a.x, a.cols, a.n2p, a.G2, a.T4, a.nchunks, a.chunk,
+             a.rows[seg], a.RT[seg], a.inv_s_scale[seg], a.xs[seg], a.cols, a.n2p, a.G2, a.T4, a.nchunks, a.chunk,
              a.cta_i0[blockIdx.x], a.cta_i1[blockIdx.x], L.rec_stride};
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   if (threadIdx.x < 20) reinterpret_cast<uint32_t*>(smem + L.bst_off)[kNW * 2 * 8 * 20 + threadIdx.x] = 0u;
@@ -947,7 +947,8 @@ int make_layout(MmaLayout& L, uint32_t rec_stride, uint32_t cols, uint32_t items
   const size_t bst_bytes = ((size_t)kNW * 2 * 8 * 20 + 20) * 4;  // B staging + a zero fragment
   const size_t rp_bytes = align16((size_t)L.items_cap * 17 * 4 + (size_t)L.items_cap * 2);
   const size_t fixed = x_bytes + part_bytes + csr_bytes + bst_bytes + rp_bytes + extra + 16 + 128 /* alignment */;
-  const size_t limit = 227 * 1024;
+  // 8 consumer warps: half an SM, so the next launch's CTA co-resides (PDL)
+  const size_t limit = (kNW <= 8 && !extra ? 112 : 227) * 1024;
   size_t S = std::min<size_t>(L.items_cap, 16);
   L.csr_nslot = 4;
   auto total_b = [&](size_t s) { return s * rec_stride + L.csr_nslot * L.csr_slot + fixed + (2 * s + 5) * 8; };
@@ -1018,21 +1019,26 @@ int plan_mma(MmaPlan& p, const DeviceLayer* const* layers, const uint32_t* const
   return opt_in_smem((const void*)mma_gemv_kernel);
 }
 
-int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
-               float* const* ys, void* stream, bool pdl, uint32_t flags) {
+int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
+               float* const* ys, void* stream, bool pdl, uint32_t flags, bool column_slots) {
   const DeviceLayer& L0 = *layers[0];
   const MmaGeometry& m = L0.mg;
   MmaArgs a;
   std::memset(&a, 0, sizeof a);
+  const size_t part_slot = (size_t)(m.nchunks + 1) * m.RT * 16;  // floats per scratch slot
   for (uint32_t l = 0; l < kMaxSeg; ++l) {
-    const DeviceLayer& L = *layers[std::min(l, n - 1)];
+    const uint32_t s = std::min(l, n - 1);
+    const DeviceLayer& L = *layers[s];
     a.recs[l] = L.mrecs, a.perm16[l] = L.perm16, a.row_ptr[l] = L.row_ptr, a.csr[l] = L.csr;
-    a.y[l] = ys[std::min(l, n - 1)];
-    a.part[l] = L.mpart, a.cnt[l] = L.mcnt;
+    a.y[l] = ys[s];
+    a.xs[l] = xs[s];
+    // the columns of one layer must not share its chunk-partial scratch
+    const uint32_t slot = column_slots ? s : 0u;
+    a.part[l] = L.mpart ? L.mpart + slot * part_slot : nullptr;
+    a.cnt[l] = L.mcnt ? L.mcnt + slot * m.RT : nullptr;
     a.rows[l] = L.g.rows, a.RT[l] = L.mg.RT;
     a.inv_s_scale[l] = 1.0f / L.plan.s_scale;
   }
-  a.x = x;
   a.cols = L0.g.cols, a.n2p = L0.g.n2p, a.G2 = L0.g.G2, a.T4 = L0.g.T4, a.nchunks = m.nchunks;
   a.wait_x = (flags & kXIndependent) ? 0u : 1u;
   a.lay = MmaLayout{p.nslot, m.rec_stride, p.x_off, p.part_off, p.csr_off, p.ent_off, p.csr_slot, p.csr_nslot,
@@ -1044,6 +1050,12 @@ int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, c
   void* params[] = {&a};
   return (int)launch_ex((const void*)mma_gemv_kernel, dim3(p.grid), dim3(kThreads), p.smem,
                         (cudaStream_t)stream, pdl, params);
+}
+
+int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
+               float* const* ys, void* stream, bool pdl, uint32_t flags) {
+  const float* xs[kMaxSeg] = {x, x, x, x};
+  return launch_mma(p, layers, n, xs, ys, stream, pdl, flags, false);
 }
 
 // ------------------------------------------------------------ decode chain

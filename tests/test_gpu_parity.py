@@ -207,8 +207,9 @@ def test_batched_tensor_core_path(rows, cols, batch):
     layer = qw.synth_layer(rows, cols, seed=rows + cols + batch, outlier_ratio=0.005)
     dl = qw.DeviceLayer(layer)
     assert dl.launches_per_matvec(batch, "gemm") == 2, "expected x prologue + tcgen05 GEMM"
-    min_b = 3 if rows * cols <= 4096 * 4096 else 4
-    assert dl.launches_per_matvec(batch) == (2 if batch >= min_b else batch)  # the default policy
+    # the default policy: K4 from 5 columns, the batch-1 kernel 4 columns to a launch below
+    assert dl.batched_path(batch) == ("gemm" if batch >= 5 else "columns")
+    assert dl.launches_per_matvec(batch) == (2 if batch >= 5 else (batch + 3) // 4)
     xs = np.stack([qw.synth_activation(cols, 300 + b) for b in range(batch)])
     Y = dl.matvec(torch.from_numpy(xs).cuda(), batched="gemm").cpu().numpy()
     assert np.all(np.isfinite(Y))
@@ -226,12 +227,43 @@ def test_batched_tensor_core_path(rows, cols, batch):
         assert rel_l2(Yc[b], oracle.matvec_f64(layer, xs[b])) <= TOL
 
 
+COLUMN_GEOMS = [
+    (96, 512, 0.01),      # one chunk, a few CTAs per column
+    (1000, 4096, 0.005),  # rows not a multiple of 16 / 4
+    (512, 11008, 0.01),   # K2m: three chunks (per-column chunk-partial slots)
+]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("rows,cols,ratio", COLUMN_GEOMS)
+def test_column_launches_match_single_columns(rows, cols, ratio, kernel):
+    """A batch on the batch-1 kernel: up to 4 columns share one launch (the
+    grid split over the columns like a layer group).  Every column equals its
+    own batch-1 launch bit for bit and the oracle within the tolerance."""
+    torch = _torch()
+    layer = qw.synth_layer(rows, cols, seed=rows + cols, outlier_ratio=ratio)
+    dl = qw.DeviceLayer(layer, kernel=kernel)
+    for batch in (2, 3, 4, 5, 7):
+        assert dl.launches_per_matvec(batch, "columns") == (batch + 3) // 4
+        xs = np.stack([qw.synth_activation(cols, 70 + b) for b in range(batch)])
+        X = torch.from_numpy(xs).cuda()
+        Y = dl.matvec(X, batched="columns").cpu().numpy()
+        Y2 = dl.matvec(X, batched="columns").cpu().numpy()
+        assert np.array_equal(Y, Y2)  # deterministic
+        for b in range(batch):
+            y1 = dl.matvec(X[b].contiguous()).cpu().numpy()
+            assert np.array_equal(Y[b].view(np.uint32), y1.view(np.uint32)), (batch, b)
+            ref = oracle.matvec_f64(layer, xs[b])
+            assert rel_l2(Y[b], ref) <= TOL
+
+
 def test_batched_unsupported_geometry_falls_back_to_columns():
     """Unpaired tiles (T2 != T4) keep the per-column fused GEMV (still exact semantics)."""
     torch = _torch()
     layer = qw.synth_layer(24, 160, seed=4, alpha=0.5)
     dl = qw.DeviceLayer(layer)
-    assert dl.launches_per_matvec(3, "gemm") == 3
+    assert dl.batched_path(3, "gemm") == "columns"
+    assert dl.launches_per_matvec(3, "gemm") == 1  # three columns, one launch
     xs = np.stack([qw.synth_activation(160, 40 + b) for b in range(3)])
     Y = dl.matvec(torch.from_numpy(xs).cuda()).cpu().numpy()
     for b in range(3):
@@ -449,7 +481,7 @@ def test_k4_a_tile_is_the_rounded_reference_weight(rows, cols, ratio):
     torch = _torch()
     layer = qw.synth_layer(rows, cols, seed=rows + 7, outlier_ratio=ratio)
     dl = qw.DeviceLayer(layer)
-    assert dl.launches_per_matvec(8) == 2, "expected the tcgen05 path"
+    assert dl.batched_path(8) == "gemm", "expected the tcgen05 path"
     P = C.c_int()
     assert qw.lib().qw_debug_gemm_shift(dl._h, C.byref(P)) == 0
     w = oracle.reconstruct_dense(layer)  # rows x padded_cols, permuted order
