@@ -117,6 +117,13 @@ def layer_paths(cache_dir: Path):
     return [cache_dir / f"{name}.qwl" for name, _, _ in SHAPES_7B]
 
 
+def ref_cache(cache_dir: Path) -> Path:
+    """Layers written only by the reference's own quantizer (oracle/_ref)."""
+    d = cache_dir / "ref"
+    d.mkdir(parents=True, exist_ok=True)
+    return d
+
+
 def ref_make_layers(cache_dir: Path):
     """The 7 distinct linears as reference PackedLayers, produced by the
     reference's OWN synth + quantize_layer (synth.cpp:11-56,
@@ -125,7 +132,7 @@ def ref_make_layers(cache_dir: Path):
     reference arm never maps this repo's library."""
     import oracle
     out = []
-    for i, ((name, rows, cols), path) in enumerate(zip(SHAPES_7B, layer_paths(cache_dir))):
+    for i, ((name, rows, cols), path) in enumerate(zip(SHAPES_7B, layer_paths(ref_cache(cache_dir)))):
         if path.exists():
             out.append(oracle.RefLayer.read(path))
             continue
@@ -139,11 +146,17 @@ def ref_make_layers(cache_dir: Path):
 
 
 def make_layers(rank: int, world: int, cache_dir: Path, threads: int):
-    """The same 7 layers for the GPU arm: read the QWL1 cache if the reference
-    arm (or an earlier run) wrote it, else produce them with this repo's
-    producer -- bit-identical to the reference's (tests/test_producer.py)."""
+    """The same 7 layers for the GPU arm: the reference-written QWL1 files if
+    the reference arm ran first on this box, else this repo's producer (its own
+    cache) -- bit-identical to the reference's (tests/test_producer.py).
+    Returns (layers, producer label)."""
     import paper_2311_16442_b200 as qw
-    paths = layer_paths(cache_dir)
+    ref_paths = layer_paths(cache_dir / "ref")
+    if all(p.exists() for p in ref_paths):
+        return [qw.read_packed_layer(str(p)) for p in ref_paths], "reference quantize_layer (QWL1 from the reference arm)"
+    own = cache_dir / "repo"
+    own.mkdir(parents=True, exist_ok=True)
+    paths = layer_paths(own)
     if rank == 0:
         for i, (name, rows, cols) in enumerate(SHAPES_7B):
             if not paths[i].exists():
@@ -154,7 +167,7 @@ def make_layers(rank: int, world: int, cache_dir: Path, threads: int):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-    return [qw.read_packed_layer(str(p)) for p in paths]
+    return [qw.read_packed_layer(str(p)) for p in paths], "repo quantize_layer (bit-identical to the reference's)"
 
 
 # --------------------------------------------------------------- CPU legs
@@ -295,7 +308,7 @@ def run_ours(args):
     cache = Path(os.environ.get("QW_BENCH_CACHE", Path(tempfile.gettempdir()) / "qw_bench_cache"))
     cache.mkdir(parents=True, exist_ok=True)
     t_prep = time.perf_counter()
-    base = make_layers(rank, world, cache, threads)
+    base, producer = make_layers(rank, world, cache, threads)
     dls = [qw.DeviceLayer(L, local, kernel=args.kernel) for L in base]
     payload = [qw.payload_bytes(L) for L in base]
     per_layer = []
@@ -501,6 +514,7 @@ def run_ours(args):
             "gpu_launches": (1 if chain else len(stack.groups)) * args.steps,
             "clocks": clocks,
             "prep_s": round(prep_s, 1),
+            "producer": producer,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
