@@ -81,6 +81,7 @@ constexpr uint32_t kDqWarps = 16;
 constexpr uint32_t kStreamMaxK = 8;       // stream-K: contributors per tile (partial slots) at most
 constexpr uint32_t kDenseStride = 20;  // fp32 words per accumulator row in shared memory
 constexpr uint32_t kThreads = (2 + kDqWarps) * 32;
+static_assert(kThreads >= 128 * 4, "split-K epilogue: one (row, 4 columns) item per thread");
 
 // ---------------------------------------------------------------- PTX
 __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
@@ -569,18 +570,32 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   } else {
     // split-K: the tile's K splits form one thread-block cluster; CTA `split`
     // sums rows [split * 128 / ks, ...) over the splits' shared-memory
-    // partials (distributed shared memory) in split order -- deterministic
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (threadIdx.x == 0) gstamp(a, 3);  // cluster joined
+    // partials (distributed shared memory) in split order -- deterministic.
+    // Split-phase cluster barriers: arrive as soon as s_dense is complete,
+    // load this thread's CSR sums (the prologue kernel's, in L2) before the
+    // wait; after the remote reads arrive again, store y, then wait (no CTA
+    // leaves while a peer may still read its shared memory).
+    // item = (row, 4 columns), one per thread (<= 128 x 4 < kThreads)
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     pdl_wait();
     if (threadIdx.x == 0) gstamp(a, 4);  // prologue kernel complete
     const uint32_t r0 = split * kTileRows / a.ks, r1 = (split + 1) * kTileRows / a.ks;
-    const uint32_t local = smem_addr(s_dense);
-    // item = (row, 4 columns): the splits' float4 partials all in flight, then
-    // summed in split order
     const uint32_t nr = r1 - r0, nc4 = (a.batch + 3) / 4;
-    for (uint32_t i = threadIdx.x; i < nr * nc4; i += blockDim.x) {
-      const uint32_t t = r0 + i % nr, c4 = i / nr, row = tile * kTileRows + t;
+    const bool item = threadIdx.x < nr * nc4;
+    const uint32_t t = r0 + (item ? threadIdx.x % nr : 0u), c4 = item ? threadIdx.x / nr : 0u;
+    const uint32_t row = tile * kTileRows + t;
+    float csr[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (item && row < G.rows) {
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k)
+        if (4 * c4 + k < a.batch) csr[k] = __ldg(a.ycsr + (size_t)(4 * c4 + k) * G.rows + row);
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (threadIdx.x == 0) gstamp(a, 3);  // cluster joined
+    float4 sum = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (item) {
+      const uint32_t local = smem_addr(s_dense);
+      // the splits' float4 partials all in flight, then summed in split order
       float4 v[8];
 #pragma unroll
       for (uint32_t sp = 0; sp < 8; ++sp) {
@@ -594,21 +609,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                        : "memory");
         }
       }
-      float4 sum = v[0];
+      sum = v[0];
 #pragma unroll
       for (uint32_t sp = 1; sp < 8; ++sp)
         if (sp < a.ks) sum.x += v[sp].x, sum.y += v[sp].y, sum.z += v[sp].z, sum.w += v[sp].w;
-      if (row < G.rows) {
-        const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+    }
+    // the remote reads are consumed: peers may leave once everyone got here
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if (item && row < G.rows) {
+      const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
 #pragma unroll
-        for (uint32_t k = 0; k < 4; ++k) {
-          const uint32_t n = 4 * c4 + k;
-          if (n < a.batch) a.y[(size_t)n * G.rows + row] = sv[k] + __ldg(a.ycsr + (size_t)n * G.rows + row);
-        }
+      for (uint32_t k = 0; k < 4; ++k) {
+        const uint32_t n = 4 * c4 + k;
+        if (n < a.batch) a.y[(size_t)n * G.rows + row] = sv[k] + csr[k];
       }
     }
     if (threadIdx.x == 0) gstamp(a, 5);  // partials summed (thread 0)
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
   if (threadIdx.x == 0) gstamp(a, 6);  // y stored
   asm volatile("tcgen05.fence::before_thread_sync;");
