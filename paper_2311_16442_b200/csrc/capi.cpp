@@ -1050,9 +1050,12 @@ int qw_debug_group_timeline(const qw_group* g, const float* x, float* const* ys,
   if (!g || !x || !ys || !stamps) return fail(QW_ERR_ARG, "timeline: null argument");
   cudaSetDevice(g->device);
   const float* xs[qwdev::kMaxSeg] = {x, x, x, x};
-  const int e = qwdev::launch_gemv_group(g->plan, g->layers.data(), (uint32_t)g->layers.size(), xs, ys, stream,
-                                         flags & 1u, (flags & 4u) ? qwdev::kXIndependent : 0u, stamps, 1,
-                                         (flags & 2u) != 0);
+  // K2m groups: %globaltimer stamps at the K2m events (qw_mma.cu)
+  const int e = g->mma ? qwdev::launch_mma(g->mplan, g->layers.data(), (uint32_t)g->layers.size(), xs, ys, stream,
+                                           flags & 1u, (flags & 4u) ? qwdev::kXIndependent : 0u, false, stamps)
+                       : qwdev::launch_gemv_group(g->plan, g->layers.data(), (uint32_t)g->layers.size(), xs, ys,
+                                                  stream, flags & 1u, (flags & 4u) ? qwdev::kXIndependent : 0u,
+                                                  stamps, 1, (flags & 2u) != 0);
   return e ? cuda_fail((cudaError_t)e, "group launch") : QW_OK;
 }
 

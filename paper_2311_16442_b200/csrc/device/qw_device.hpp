@@ -220,7 +220,8 @@ int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, c
                float* const* ys, void* stream, bool pdl, uint32_t flags);
 // segment s reads xs[s]; column_slots: segment s uses the layer's scratch slot s
 int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
-               float* const* ys, void* stream, bool pdl, uint32_t flags, bool column_slots);
+               float* const* ys, void* stream, bool pdl, uint32_t flags, bool column_slots,
+               unsigned long long* dbg = nullptr);
 
 // Decode chain (batch 1): a sequence of launch steps (each a group of 1..4
 // layers of identical geometry reading one activation) run by ONE persistent

@@ -103,6 +103,7 @@ namespace {
 
 constexpr uint32_t kNW = QW_MMA_NW;             // consumer warps
 constexpr uint32_t kThreads = (kNW + 2) * 32;   // + producer + CSR warp
+constexpr uint32_t kCsrSlotsMax = 16;            // CSR ring: a power of two <= this many tile spans in flight
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
@@ -299,7 +300,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // maximum over its steps).
 struct MmaLayout {
   uint32_t S, rec_stride, x_off, part_off, csr_off, ent_off, csr_slot, csr_nslot, rp_off, bst_off, bar_off,
-      items_cap, diag;
+      items_cap, diag, x_gate;
 };
 
 // One step (a layer group sharing x) as one CTA sees it.
@@ -337,6 +338,7 @@ struct MmaArgs {
   MmaChunk chunk[kMmaMaxChunks];
   uint8_t cta_seg[kMaxGrid];
   uint32_t cta_i0[kMaxGrid], cta_i1[kMaxGrid];
+  unsigned long long* dbg;  // diagnostics: [grid][kTimelineEvents] %globaltimer stamps (or null)
 };
 
 // Persistent decode chain: per step (global memory) ...
@@ -381,7 +383,8 @@ struct MmaState {
 };
 
 __device__ __forceinline__ void producer_step(const StepView& v, const MmaLayout& L, uint8_t* smem, uint64_t* full,
-                                              uint64_t* empty, MmaState& st, uint32_t& issued) {
+                                              uint64_t* empty, MmaState& st, uint32_t& issued,
+                                              uint64_t* xbar = nullptr, uint32_t x_gate = 0) {
   const uint32_t nitems = v.i1 - v.i0;
   if (!nitems) return;
   const uint32_t RT = v.RT;
@@ -389,6 +392,9 @@ __device__ __forceinline__ void producer_step(const StepView& v, const MmaLayout
   const uint32_t n = (L.diag & 1) ? min(nitems, L.S) : nitems;
   for (uint32_t k = 0; k < n; ++k) {
     const uint32_t bytes = v.chunk[ch].rec_bytes;
+    // hold the stream after x_gate records until x is staged: the x loads
+    // then meet a quieter memory system (they sit on the critical path)
+    if (xbar && k == x_gate) mbar_wait(xbar, 0);
     if (issued >= L.S) mbar_wait_spin(&empty[st.slot], st.phase ^ 1u);  // no suspend: refill at once
     mbar_expect_tx(&full[st.slot], bytes);
     bulk_load_nohint(smem + (size_t)st.slot * L.rec_stride, v.recs + (size_t)(v.i0 + k) * v.hbm_stride, bytes,
@@ -429,14 +435,32 @@ __device__ __forceinline__ void csr_prepare(const StepView& v, const MmaLayout& 
   uint16_t* s_qk = reinterpret_cast<uint16_t*>(s_rp + L.items_cap * 17);  // item of CSR item q
   nq = 0;
   if (!(L.diag & 4) && nitems) {
+    // the CSR items (tiles this CTA sums) first, then their row_ptr words
+    // with 8 loads in flight per lane (one load per item in a dependent
+    // sequence cost a memory latency per item: 7 us for 9 items)
     uint32_t ch = v.i0 / RT, tile = v.i0 - ch * RT;
     for (uint32_t k = 0; k < nitems; ++k) {
       if (tile % nch == ch) {
-        if (lane <= 16) s_rp[nq * 17 + lane] = __ldg(rp + min(tile * 16 + lane, rows));
         if (lane == 0) s_qk[nq] = (uint16_t)k;
         ++nq;
       }
       if (++tile == RT) tile = 0, ++ch;
+    }
+    __syncwarp();
+    const uint32_t nw = nq * 17;
+    for (uint32_t base = 0; base < nw; base += 8 * 32) {
+      uint32_t w[8];
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) {
+        const uint32_t f = base + u * 32 + lane;
+        if (f < nw) {
+          const uint32_t q = f / 17, j = f - q * 17, t = (v.i0 + s_qk[q]) % RT;
+          w[u] = __ldg(rp + min(t * 16 + j, rows));
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u)
+        if (base + u * 32 + lane < nw) s_rp[base + u * 32 + lane] = w[u];
     }
   }
   __syncwarp();
@@ -457,7 +481,7 @@ __device__ __forceinline__ void csr_compute(const StepView& v, const MmaLayout& 
   const uint32_t* __restrict__ ent = v.csr;
   const uint32_t* s_rp = reinterpret_cast<const uint32_t*>(smem + L.rp_off);
   const uint16_t* s_qk = reinterpret_cast<const uint16_t*>(s_rp + L.items_cap * 17);
-  const uint32_t CS = L.csr_nslot, cmask = CS - 1, csh = CS == 4 ? 2 : 1, q0 = st.q;
+  const uint32_t CS = L.csr_nslot, cmask = CS - 1, csh = __ffs(CS) - 1, q0 = st.q;
   mbar_wait(xbar, xphase);
   const uint32_t r = lane & 15u, half = lane >> 4, nst = L.csr_slot / 4;
   for (uint32_t q = 0; q < nq; ++q) {
@@ -537,7 +561,8 @@ __device__ __forceinline__ void consumer_step(const StepView& v, const MmaLayout
                                               uint64_t* empty, uint64_t* xbar, uint32_t xphase, float* s_x,
                                               float* s_part, float* s_csr, MmaState& st, uint32_t warp,
                                               uint32_t lane, bool wait_pdl, WarpBlocks& wb, bool prefetched,
-                                              const StepView* next, unsigned long long* tl = nullptr) {
+                                              const StepView* next, unsigned long long* tl = nullptr,
+                                              bool per_launch = false) {
   const uint32_t g = lane >> 2, t = lane & 3u;
   const bool nz = t == (g >> 1);  // this lane holds column g of the block-diagonal B
   // B staging (cooperative build): lane (n = lane / 4, quarter c = lane % 4)
@@ -552,6 +577,7 @@ __device__ __forceinline__ void consumer_step(const StepView& v, const MmaLayout
   if (nitems && !prefetched) fetch_perm(v.i0 / RT);
   // x -> shared memory (coalesced), the pads' zero slot at cols
   if (wait_pdl) pdl_wait();
+  if (per_launch && tl && threadIdx.x == 0) tl[10] = gtimer();  // dependency resolved
   {
     const uint32_t tid = threadIdx.x, nth = kNW * 32, cols = v.cols;
     if ((((uintptr_t)v.x) & 15u) == 0 && (cols & 3u) == 0) {
@@ -640,6 +666,7 @@ __device__ __forceinline__ void consumer_step(const StepView& v, const MmaLayout
   uint32_t ch = nitems ? v.i0 / RT : 0u, k = 0;
   while (k < nitems) {
     build_b();
+    if (per_launch && tl && threadIdx.x == 0 && k == 0) tl[11] = gtimer();  // first B built
     // the items of this chunk, one warp-role specialised loop (no per-item dispatch)
     const uint32_t kend = min(nitems, k + (RT - (v.i0 + k - ch * RT)));
     const float2 ys = make_float2(ys2, ys4);
@@ -681,6 +708,7 @@ __device__ __forceinline__ void consumer_step(const StepView& v, const MmaLayout
       if (c == tile % nch) v.part[(size_t)nch * RT * 16 + row] = s_csr[idx];
     }
   }
+  if (per_launch && tl && threadIdx.x == 0) tl[9] = gtimer();  // dense sums stored (thread 0)
   if (nch == 1 || (L.diag & 8)) return;
   // chunk partials meet: the last arriving CTA of a tile sums them in chunk
   // order (CTA barrier, then lane 0's acq_rel atomic: cumulative release of
@@ -711,10 +739,10 @@ __device__ __forceinline__ uint8_t* aligned_smem(uint8_t* raw) {
   return raw + ((128u - (smem_addr(raw) & 127u)) & 127u);
 }
 __device__ __forceinline__ void init_barriers(uint64_t* bars, uint32_t S) {
-  // [0, S) full, [S, 2S) empty, 2S x staged, 2S+1 .. 2S+4 CSR ring
+  // [0, S) full, [S, 2S) empty, 2S x staged, 2S+1 .. 2S+kCsrSlotsMax CSR ring
   if (threadIdx.x < S) mbar_init(&bars[threadIdx.x], 1), mbar_init(&bars[S + threadIdx.x], kNW);
   if (threadIdx.x == 32) mbar_init(&bars[2 * S], kNW);
-  if (threadIdx.x >= 64 && threadIdx.x < 68) mbar_init(&bars[2 * S + 1 + (threadIdx.x - 64)], 1);
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + kCsrSlotsMax) mbar_init(&bars[2 * S + 1 + (threadIdx.x - 64)], 1);
 }
 
 __global__ void __launch_bounds__(kThreads, kNW <= 8 ? 2 : 1) mma_gemv_kernel(const __grid_constant__ MmaArgs a) {
@@ -727,6 +755,8 @@ __global__ void __launch_bounds__(kThreads, kNW <= 8 ? 2 : 1) mma_gemv_kernel(co
              a.rows[seg], a.RT[seg], a.inv_s_scale[seg], a.xs[seg], a.cols, a.n2p, a.G2, a.T4, a.nchunks, a.chunk,
              a.cta_i0[blockIdx.x], a.cta_i1[blockIdx.x], L.rec_stride};
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  unsigned long long* tl = a.dbg ? a.dbg + (size_t)blockIdx.x * kTimelineEvents : nullptr;
+  if (tl && threadIdx.x == 0) tl[0] = gtimer();  // entry
   if (threadIdx.x < 20) reinterpret_cast<uint32_t*>(smem + L.bst_off)[kNW * 2 * 8 * 20 + threadIdx.x] = 0u;
   init_barriers(bars, L.S);
   mbar_fence_init();
@@ -737,19 +767,23 @@ __global__ void __launch_bounds__(kThreads, kNW <= 8 ? 2 : 1) mma_gemv_kernel(co
   float* s_csr = reinterpret_cast<float*>(smem + L.csr_off);
   if (warp == kNW) {  // producer: the weight stream never waits on x
     uint32_t issued = 0;
-    if (lane == 0) producer_step(v, L, smem, bars, bars + L.S, st, issued);
+    if (lane == 0) producer_step(v, L, smem, bars, bars + L.S, st, issued, L.x_gate ? bars + 2 * L.S : nullptr, L.x_gate);
+    if (tl && lane == 0) tl[7] = gtimer();  // every copy issued
     return;
   }
   if (warp == kNW + 1) {
     uint32_t nq = 0;
     csr_prepare(v, L, smem, bars + 2 * L.S + 1, st, lane, nq);
+    if (tl && lane == 0) tl[8] = gtimer();  // CSR spans requested
     csr_compute(v, L, smem, bars + 2 * L.S, 0u, bars + 2 * L.S + 1, s_x, s_csr, st, lane, nq);
+    if (tl && lane == 0) tl[6] = gtimer();  // outlier sums done
     named_sync(1, (kNW + 1) * 32);
     return;
   }
   WarpBlocks wb;
   consumer_step(v, L, smem, bars, bars + L.S, bars + 2 * L.S, 0u, s_x, reinterpret_cast<float*>(smem + L.part_off),
-                s_csr, st, warp, lane, a.wait_x != 0, wb, false, nullptr);
+                s_csr, st, warp, lane, a.wait_x != 0, wb, false, nullptr, tl, true);
+  if (tl && threadIdx.x == 0) tl[5] = gtimer();  // y / partials stored, fixup done (thread 0)
 }
 
 // The whole decode step as ONE persistent kernel (one CTA per SM): the
@@ -765,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1) mma_chain_kernel(const __grid_con
   const MmaLayout& L = a.lay;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
-  StepView* s_view = reinterpret_cast<StepView*>(smem + L.bar_off + ((2 * L.S + 5) * 8 + 15) / 16 * 16);
+  StepView* s_view = reinterpret_cast<StepView*>(smem + L.bar_off + ((2 * L.S + 1 + kCsrSlotsMax) * 8 + 15) / 16 * 16);
   auto load_view = [&](uint32_t s, StepView& out) {
     const MmaStepDesc& d = a.steps[s];
     const MmaCtaRange r = a.ranges[(size_t)s * a.grid + blockIdx.x];
@@ -950,10 +984,17 @@ int make_layout(MmaLayout& L, uint32_t rec_stride, uint32_t cols, uint32_t items
   // 8 consumer warps: half an SM, so the next launch's CTA co-resides (PDL)
   const size_t limit = (kNW <= 8 && !extra ? 112 : 227) * 1024;
   size_t S = std::min<size_t>(L.items_cap, 16);
-  L.csr_nslot = 4;
-  auto total_b = [&](size_t s) { return s * rec_stride + L.csr_nslot * L.csr_slot + fixed + (2 * s + 5) * 8; };
+  // CSR ring: every tile span of the CTA in flight at once when it fits (a
+  // span refilled only after an earlier one was summed costs a memory
+  // latency on the CSR warp's critical path)
+  L.csr_nslot = 2;
+  while (L.csr_nslot < kCsrSlotsMax && L.csr_nslot < L.items_cap && L.csr_nslot * 2 * L.csr_slot <= 48 * 1024)
+    L.csr_nslot *= 2;
+  auto total_b = [&](size_t s) {
+    return s * rec_stride + L.csr_nslot * L.csr_slot + fixed + (2 * s + 1 + kCsrSlotsMax) * 8;
+  };
   while (S > 2 && total_b(S) > limit) --S;
-  if (total_b(S) > limit) L.csr_nslot = 2;  // shallower CSR ring
+  while (total_b(S) > limit && L.csr_nslot > 2) L.csr_nslot /= 2;  // shallower CSR ring
   while (total_b(S) > limit && L.csr_slot > 1024) L.csr_slot = L.csr_slot / 2 & ~15u;  // rest from global
   if (total_b(S) > limit) return (int)cudaErrorInvalidConfiguration;
   L.S = (uint32_t)S;
@@ -964,7 +1005,7 @@ int make_layout(MmaLayout& L, uint32_t rec_stride, uint32_t cols, uint32_t items
   L.rp_off = L.ent_off + L.csr_nslot * L.csr_slot;
   L.bst_off = L.rp_off + (uint32_t)rp_bytes;
   L.bar_off = L.bst_off + (uint32_t)bst_bytes;
-  smem = L.bar_off + (uint32_t)(((2 * S + 5) * 8 + 15) / 16 * 16 + extra) + 128;
+  smem = L.bar_off + (uint32_t)(((2 * S + 1 + kCsrSlotsMax) * 8 + 15) / 16 * 16 + extra) + 128;
   return 0;
 }
 
@@ -1020,7 +1061,8 @@ int plan_mma(MmaPlan& p, const DeviceLayer* const* layers, const uint32_t* const
 }
 
 int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
-               float* const* ys, void* stream, bool pdl, uint32_t flags, bool column_slots) {
+               float* const* ys, void* stream, bool pdl, uint32_t flags, bool column_slots,
+               unsigned long long* dbg) {
   const DeviceLayer& L0 = *layers[0];
   const MmaGeometry& m = L0.mg;
   MmaArgs a;
@@ -1042,11 +1084,13 @@ int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, c
   a.cols = L0.g.cols, a.n2p = L0.g.n2p, a.G2 = L0.g.G2, a.T4 = L0.g.T4, a.nchunks = m.nchunks;
   a.wait_x = (flags & kXIndependent) ? 0u : 1u;
   a.lay = MmaLayout{p.nslot, m.rec_stride, p.x_off, p.part_off, p.csr_off, p.ent_off, p.csr_slot, p.csr_nslot,
-                    p.rp_off, p.bst_off, p.bar_off, p.items_max, diag_flags()};
+                    p.rp_off, p.bst_off, p.bar_off, p.items_max, diag_flags(),
+                    (flags & kXIndependent) ? 0u : qwdev::knob("QW_MMA_XGATE", 0)};
   for (uint32_t c = 0; c < kMmaMaxChunks; ++c) a.chunk[c] = m.chunk[c];
   std::copy(p.cta_seg, p.cta_seg + p.grid, a.cta_seg);
   std::copy(p.cta_i0, p.cta_i0 + p.grid, a.cta_i0);
   std::copy(p.cta_i1, p.cta_i1 + p.grid, a.cta_i1);
+  a.dbg = dbg;
   void* params[] = {&a};
   return (int)launch_ex((const void*)mma_gemv_kernel, dim3(p.grid), dim3(kThreads), p.smem,
                         (cudaStream_t)stream, pdl, params);
@@ -1055,7 +1099,7 @@ int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, c
 int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
                float* const* ys, void* stream, bool pdl, uint32_t flags) {
   const float* xs[kMaxSeg] = {x, x, x, x};
-  return launch_mma(p, layers, n, xs, ys, stream, pdl, flags, false);
+  return launch_mma(p, layers, n, xs, ys, stream, pdl, flags, false, nullptr);
 }
 
 // ------------------------------------------------------------ decode chain
