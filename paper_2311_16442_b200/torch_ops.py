@@ -18,10 +18,11 @@ import itertools
 
 import torch
 
-from .engine import DeviceLayer
+from .engine import DeviceLayer, LayerGroup
 from .layer import PackedLayer
 
 _REGISTRY: dict[int, DeviceLayer] = {}
+_GROUPS: dict[int, LayerGroup] = {}
 _IDS = itertools.count(1)
 
 
@@ -35,13 +36,54 @@ def quantized_linear(x: torch.Tensor, layer_id: int) -> torch.Tensor:
         return x.new_empty((*lead, dl.rows))
     ys = []
     for c0 in range(0, xb.shape[0], 16):  # the batched path takes at most 16 columns per call
-        ys.append(dl.matvec(xb[c0:c0 + 16]))
+        # programmatic dependent launch: the weight stream starts under the
+        # previous kernel on the stream; x is read after it completes
+        ys.append(dl.matvec(xb[c0:c0 + 16], pdl=True))
     return torch.cat(ys, 0).reshape(*lead, dl.rows)
 
 
 @quantized_linear.register_fake
 def _(x: torch.Tensor, layer_id: int) -> torch.Tensor:
     return x.new_empty((*x.shape[:-1], _REGISTRY[layer_id].rows))
+
+
+@torch.library.custom_op("qweight_b200::quantized_linear_group", mutates_args=())
+def quantized_linear_group(x: torch.Tensor, group_id: int) -> list[torch.Tensor]:
+    """[W_i x for each layer of the registered group]: batch 1 is ONE fused
+    launch for all the layers (q/k/v, gate/up: one dependency wait, one
+    activation staging); larger batches run each layer's batched path."""
+    grp = _GROUPS[group_id]
+    lead = x.shape[:-1]
+    xb = x.reshape(-1, x.shape[-1]).contiguous()
+    if xb.shape[0] == 1:
+        return [y.reshape(*lead, y.shape[0]) for y in grp.matvec(xb.reshape(-1), pdl=True)]
+    return [quantized_linear(x, lid) for lid in grp.layer_ids]
+
+
+@quantized_linear_group.register_fake
+def _(x: torch.Tensor, group_id: int) -> list[torch.Tensor]:
+    return [x.new_empty((*x.shape[:-1], _REGISTRY[lid].rows)) for lid in _GROUPS[group_id].layer_ids]
+
+
+class QuantizedLinearGroup(torch.nn.Module):
+    """Several nn.Linear-shaped layers that read the same input (q/k/v,
+    gate/up), computed by one fused launch at batch 1.  forward(x) returns
+    the tuple of outputs."""
+
+    def __init__(self, layers: list, device: int = 0, kernel: str = "auto"):
+        super().__init__()
+        self.members = torch.nn.ModuleList(QuantizedLinear(l, device, kernel) for l in layers)
+        self.group = LayerGroup([m.dl for m in self.members])
+        self.group.layer_ids = [m.layer_id for m in self.members]
+        self.group_id = next(_IDS)
+        _GROUPS[self.group_id] = self.group
+
+    def forward(self, x: torch.Tensor):
+        return tuple(torch.ops.qweight_b200.quantized_linear_group(x, self.group_id))
+
+    def __del__(self):
+        if _GROUPS is not None:
+            _GROUPS.pop(getattr(self, "group_id", None), None)
 
 
 class QuantizedLinear(torch.nn.Module):
@@ -63,4 +105,5 @@ class QuantizedLinear(torch.nn.Module):
                 f"kernel={'K2m' if self.dl.uses_tensor_core else 'K2'}")
 
     def __del__(self):
-        _REGISTRY.pop(getattr(self, "layer_id", None), None)
+        if _REGISTRY is not None:  # (interpreter shutdown clears module globals)
+            _REGISTRY.pop(getattr(self, "layer_id", None), None)

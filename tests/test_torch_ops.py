@@ -41,3 +41,32 @@ def test_quantized_linear_module_eager_graph_compile():
     yl = mlp[0](xl.reshape(4, 5, 1024))
     assert yl.shape == (4, 5, 512)
     assert rel_l2(yl.reshape(20, 512)[17].cpu().numpy(), oracle.matvec_f64(layers[0], xl[17].cpu().numpy())) <= 1e-2
+
+
+def test_quantized_linear_group_module():
+    """q/k/v as one QuantizedLinearGroup: one fused launch at batch 1 (also
+    under CUDA-graph capture), each layer's batched path above; every output
+    matches its own QuantizedLinear and the f64 oracle."""
+    import torch
+    from paper_2311_16442_b200.torch_ops import QuantizedLinear, QuantizedLinearGroup
+    layers = [qw.synth_layer(r, 1024, seed=40 + i, outlier_ratio=0.005) for i, r in enumerate((512, 256, 256))]
+    grp = QuantizedLinearGroup(layers)
+    singles = [QuantizedLinear(m.dl) for m in grp.members]
+    for b in (1, 3):
+        x = torch.from_numpy(np.stack([qw.synth_activation(1024, 50 + i) for i in range(b)])).cuda()
+        outs = grp(x)
+        assert [o.shape for o in outs] == [(b, 512), (b, 256), (b, 256)]
+        for L, o, m in zip(layers, outs, singles):
+            ref_single = m(x)
+            assert float((o - ref_single).abs().max()) <= 1e-6 * float(ref_single.abs().max())
+            for i in range(b):
+                assert rel_l2(o[i].cpu().numpy(), oracle.matvec_f64(L, x[i].cpu().numpy())) <= 1e-2
+    # batch 1 under CUDA-graph capture
+    x1 = torch.from_numpy(qw.synth_activation(1024, 70)).cuda().reshape(1, 1024)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        outs = grp(x1)
+    g.replay()
+    torch.cuda.synchronize()
+    for o, e in zip(outs, grp(x1)):
+        assert torch.equal(o, e)
