@@ -212,17 +212,17 @@ int qw_matvec_pdl(const qw_layer* layer, const float* x, uint32_t batch,
                                       reading it (q/k/v, gate/up share inputs) */
 /* Batched calls (batch >= 2): by default batch >= QW_GEMM_MIN_BATCH runs the
  * tcgen05 GEMM K4; smaller batches run the batch-1 kernel over the columns,
- * up to 4 columns sharing one launch (the grid split over the columns, each
+ * up to 8 columns sharing one launch (the grid split over the columns, each
  * column's result bit-identical to its own batch-1 call; the weights are
  * read from HBM about once and shared through L2).  The crossover is
  * measured (profiles/r02_batch_sweep_*.jsonl).  These flags force one or the
  * other. */
-#define QW_GEMM_MIN_BATCH 5u
+#define QW_GEMM_MIN_BATCH 7u
 #define QW_LAUNCH_FORCE_GEMM 4u
 #define QW_LAUNCH_FORCE_COLUMNS 8u
 int qw_matvec_ex(const qw_layer* layer, const float* x, uint32_t batch, float* y,
                  qw_workspace* ws, void* stream, uint32_t flags);
-/* Group launch (batch 1): up to 4 layers that read the same activation
+/* Group launch (batch 1): up to 8 layers that read the same activation
  * (q/k/v, gate/up) in ONE fused launch -- one dependency wait, one activation
  * staging.  The layers share cols, channel split and group2; rows may differ
  * (GQA q/k/v).  The layers must outlive the group.
@@ -240,7 +240,7 @@ int qw_group_matvec(const qw_group* group, const float* x, float* const* ys, voi
 int qw_layer_set_prefetch(qw_layer* layer, const qw_layer* const* next, uint32_t n);
 int qw_group_set_prefetch(qw_group* group, const qw_layer* const* next, uint32_t n);
 /* Decode chain (batch 1): a fixed sequence of launch steps -- each a group of
- * 1..4 layers of identical geometry reading one activation x -- executed by
+ * 1..8 layers of identical geometry reading one activation x -- executed by
  * ONE persistent kernel: one CTA per SM streams the packed weights of all
  * steps through a single shared-memory ring (step s+1's weights land while
  * step s computes), and a step with depends != 0 reads x only after every CTA

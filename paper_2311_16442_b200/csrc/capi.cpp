@@ -334,8 +334,8 @@ int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
 }
 
 // batched policy (qweight_b200.h): K4 from QW_GEMM_MIN_BATCH columns up, the
-// batch-1 kernel over the columns (4 to a launch) below -- at 2..4 columns
-// one column launch beats K4's fixed cost on every 7B shape
+// batch-1 kernel over the columns (8 to a launch) below -- up to 6 columns
+// one column launch beats K4's fixed cost on q/gate/up, up to 5 on down
 // (profiles/r02_batch_sweep_simt.jsonl)
 bool uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
   static const uint32_t forced = qwdev::knob("QW_GEMM_MIN_BATCH", 0);
@@ -894,7 +894,7 @@ int qw_debug_timeline(const qw_layer* L, const float* x, float* y, unsigned long
 int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out) {
   return guarded([&] {
     if (!layers || !out || n == 0) return fail(QW_ERR_ARG, "group: null argument");
-    if (n > qwdev::kMaxSeg) return fail(QW_ERR_UNSUPPORTED, "group: at most 4 layers");
+    if (n > qwdev::kMaxSeg) return fail(QW_ERR_UNSUPPORTED, "group: at most 8 layers");
     auto G = std::make_unique<qw_group>();
     std::vector<const uint32_t*> rps;
     for (uint32_t i = 0; i < n; ++i) {
@@ -985,7 +985,7 @@ int qw_chain_create(const qw_chain_step* steps, uint32_t n, qw_chain** out) {
     for (uint32_t s = 0; s < n; ++s) {
       const qw_chain_step& st = steps[s];
       if (!st.layers || !st.ys || !st.x || st.n == 0) return fail(QW_ERR_ARG, "chain: null step field");
-      if (st.n > qwdev::kMaxSeg) return fail(QW_ERR_UNSUPPORTED, "chain: at most 4 layers per step");
+      if (st.n > qwdev::kMaxSeg) return fail(QW_ERR_UNSUPPORTED, "chain: at most 8 layers per step");
       for (uint32_t l = 0; l < st.n; ++l) {
         if (!st.layers[l] || !st.ys[l]) return fail(QW_ERR_ARG, "chain: null layer or output");
         if (st.layers[l]->device != device) return fail(QW_ERR_ARG, "chain: layers on different devices");
@@ -1049,7 +1049,8 @@ int qw_debug_group_timeline(const qw_group* g, const float* x, float* const* ys,
                             uint32_t flags, void* stream) {
   if (!g || !x || !ys || !stamps) return fail(QW_ERR_ARG, "timeline: null argument");
   cudaSetDevice(g->device);
-  const float* xs[qwdev::kMaxSeg] = {x, x, x, x};
+  const float* xs[qwdev::kMaxSeg];
+  std::fill(xs, xs + qwdev::kMaxSeg, x);
   // K2m groups: %globaltimer stamps at the K2m events (qw_mma.cu)
   const int e = g->mma ? qwdev::launch_mma(g->mplan, g->layers.data(), (uint32_t)g->layers.size(), xs, ys, stream,
                                            flags & 1u, (flags & 4u) ? qwdev::kXIndependent : 0u, false, stamps)

@@ -3,7 +3,7 @@
 // The reference computes a batch as independent GEMVs (one matvec per
 // activation, engine.cpp:169-249).  Running the batch-1 kernel once per
 // column pays the per-launch cost b times; K4 (qw_gemm.cu) pays ~7 us of
-// fixed cost.  Here up to kMaxSeg columns share ONE launch: the grid is split
+// fixed cost.  Here up to kMaxSeg (8) columns share ONE launch: the grid is split
 // over the columns exactly like a layer group (qw_gemv.cu / qw_mma.cu group
 // launches), every segment the same layer with its own x and y.  The
 // segments' CTAs stream the same records at the same time, so HBM delivers
@@ -18,8 +18,10 @@
 namespace qwdev {
 
 int plan_columns(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
-  const DeviceLayer* same[kMaxSeg] = {&L, &L, &L, &L};
-  const uint32_t* rps[kMaxSeg] = {host_row_ptr, host_row_ptr, host_row_ptr, host_row_ptr};
+  const DeviceLayer* same[kMaxSeg];
+  const uint32_t* rps[kMaxSeg];
+  std::fill(same, same + kMaxSeg, &L);
+  std::fill(rps, rps + kMaxSeg, host_row_ptr);
   for (uint32_t n = 2; n <= kMaxSeg; ++n) {
     GemvPlan& p = L.cplan[n - 2];
     if (plan_gemv_group(p, same, rps, n, num_sms)) p = GemvPlan{}, p.grid = 0;  // per-column fallback
@@ -32,7 +34,8 @@ int plan_columns(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
 
 int launch_columns(const DeviceLayer& L, const float* x, uint32_t batch, float* y, void* stream, bool pdl,
                    uint32_t flags) {
-  const DeviceLayer* same[kMaxSeg] = {&L, &L, &L, &L};
+  const DeviceLayer* same[kMaxSeg];
+  std::fill(same, same + kMaxSeg, &L);
   for (uint32_t c0 = 0; c0 < batch;) {
     const uint32_t n = std::min<uint32_t>(kMaxSeg, batch - c0);
     const float* xs[kMaxSeg];

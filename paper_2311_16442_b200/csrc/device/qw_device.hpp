@@ -84,7 +84,7 @@ struct GemvPlan {
 // same activation (q/k/v, gate/up); the CTAs are split across the layers in
 // proportion to their quads and each CTA owns a quad range of one layer, so
 // the dependency wait, the activation staging and the launch are paid once.
-constexpr uint32_t kMaxSeg = 4;
+constexpr uint32_t kMaxSeg = 8;
 
 // Batched (2..16 columns) tensor-core plan: 128-row M tiles x KS K splits of
 // 2-tile stages (96 2-bit + 32 4-bit channels); TMA 2-D boxes of the quad

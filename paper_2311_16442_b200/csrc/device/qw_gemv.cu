@@ -993,7 +993,8 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
 
 int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
                       float* const* ys, void* stream, bool pdl, uint32_t flags) {
-  const float* xs[kMaxSeg] = {x, x, x, x};
+  const float* xs[kMaxSeg];
+  std::fill(xs, xs + kMaxSeg, x);
   return launch_gemv_group(p, layers, n, xs, ys, stream, pdl, flags, nullptr, 1, false);
 }
 

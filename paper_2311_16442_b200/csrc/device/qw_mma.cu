@@ -1098,7 +1098,8 @@ int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, c
 
 int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
                float* const* ys, void* stream, bool pdl, uint32_t flags) {
-  const float* xs[kMaxSeg] = {x, x, x, x};
+  const float* xs[kMaxSeg];
+  std::fill(xs, xs + kMaxSeg, x);
   return launch_mma(p, layers, n, xs, ys, stream, pdl, flags, false, nullptr);
 }
 

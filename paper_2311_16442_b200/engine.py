@@ -151,9 +151,9 @@ class DeviceLayer:
             raise QWeightError(1, "matvec: out must be a contiguous cuda float32 tensor of batch * rows "
                                   "elements on the activation's device")
         ws = workspace or default_workspace(self.device)
-        # batched: "auto" (K4 from 5 columns, the batch-1 kernel over the
+        # batched: "auto" (K4 from 7 columns, the batch-1 kernel over the
         # columns below), "gemm" (force the tcgen05 GEMM K4), "columns"
-        # (force the batch-1 kernel, up to 4 columns per launch)
+        # (force the batch-1 kernel, up to 8 columns per launch)
         flags = (1 if pdl else 0) | (2 if x_independent else 0) | {"auto": 0, "gemm": 4, "columns": 8}[batched]
         check(lib().qw_matvec_ex(self._h, C.c_void_p(xb.data_ptr()), batch,
                                  C.c_void_p(out.data_ptr()), ws._h,
@@ -235,7 +235,7 @@ class DeviceLayer:
 
     def batched_path(self, batch: int, batched: str = "auto") -> str:
         """"gemm" (the tcgen05 GEMM K4) or "columns" (the batch-1 kernel over
-        the columns, up to 4 per launch) for a matvec of `batch` columns."""
+        the columns, up to 8 per launch) for a matvec of `batch` columns."""
         r = lib().qw_matvec_uses_gemm(self._h, batch, {"auto": 0, "gemm": 4, "columns": 8}[batched])
         if r < 0:
             check(r)

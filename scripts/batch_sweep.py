@@ -1,6 +1,6 @@
 """BASELINE config 3: Llama-2-7B shapes, batch 1/2/3/4/8/16: the batched
 policy against both forced paths (K4 tcgen05 GEMM; the batch-1 kernel over
-the columns, up to 4 columns per launch).  Per-call time from a CUDA-graph
+the columns, up to 8 columns per launch).  Per-call time from a CUDA-graph
 chain of N distinct layer copies (inputs > L2).  With QW_DEBUG_KNOBS=1
 QW_COLUMN_GROUP=0 the column path runs one launch per column (A/B).
 usage: python scripts/batch_sweep.py [N] [nopdl] [simt|mma|auto]  -> one JSON line per (shape, batch, path)"""
@@ -24,7 +24,7 @@ for name, rows, cols in (("q_proj", 4096, 4096), ("gate_proj", 11008, 4096), ("d
     base = qw.DeviceLayer(layer, kernel=KERNEL)
     dls = [base] + [base.clone() for _ in range(N - 1)]
     payload = qw.payload_bytes(layer)
-    for b, mode in [(1, "auto")] + [(b, m) for b in (2, 3, 4, 8, 16) for m in ("auto", "gemm", "columns")]:
+    for b, mode in [(1, "auto")] + [(b, m) for b in (2, 3, 4, 5, 6, 7, 8, 16) for m in ("auto", "gemm", "columns")]:
         xs = torch.from_numpy(np.stack([qw.synth_activation(cols, 50 + i) for i in range(b)])).cuda()
         ys = torch.empty(N, b, rows, device="cuda")
 

@@ -207,9 +207,9 @@ def test_batched_tensor_core_path(rows, cols, batch):
     layer = qw.synth_layer(rows, cols, seed=rows + cols + batch, outlier_ratio=0.005)
     dl = qw.DeviceLayer(layer)
     assert dl.launches_per_matvec(batch, "gemm") == 2, "expected x prologue + tcgen05 GEMM"
-    # the default policy: K4 from 5 columns, the batch-1 kernel 4 columns to a launch below
-    assert dl.batched_path(batch) == ("gemm" if batch >= 5 else "columns")
-    assert dl.launches_per_matvec(batch) == (2 if batch >= 5 else (batch + 3) // 4)
+    # the default policy: K4 from 7 columns, the batch-1 kernel 8 columns to a launch below
+    assert dl.batched_path(batch) == ("gemm" if batch >= 7 else "columns")
+    assert dl.launches_per_matvec(batch) == (2 if batch >= 7 else (batch + 7) // 8)
     xs = np.stack([qw.synth_activation(cols, 300 + b) for b in range(batch)])
     Y = dl.matvec(torch.from_numpy(xs).cuda(), batched="gemm").cpu().numpy()
     assert np.all(np.isfinite(Y))
@@ -237,14 +237,14 @@ COLUMN_GEOMS = [
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("rows,cols,ratio", COLUMN_GEOMS)
 def test_column_launches_match_single_columns(rows, cols, ratio, kernel):
-    """A batch on the batch-1 kernel: up to 4 columns share one launch (the
+    """A batch on the batch-1 kernel: up to 8 columns share one launch (the
     grid split over the columns like a layer group).  Every column equals its
     own batch-1 launch bit for bit and the oracle within the tolerance."""
     torch = _torch()
     layer = qw.synth_layer(rows, cols, seed=rows + cols, outlier_ratio=ratio)
     dl = qw.DeviceLayer(layer, kernel=kernel)
-    for batch in (2, 3, 4, 5, 7):
-        assert dl.launches_per_matvec(batch, "columns") == (batch + 3) // 4
+    for batch in (2, 3, 5, 8, 11):
+        assert dl.launches_per_matvec(batch, "columns") == (batch + 7) // 8
         xs = np.stack([qw.synth_activation(cols, 70 + b) for b in range(batch)])
         X = torch.from_numpy(xs).cuda()
         Y = dl.matvec(X, batched="columns").cpu().numpy()
