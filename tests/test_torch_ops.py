@@ -70,3 +70,7 @@ def test_quantized_linear_group_module():
     torch.cuda.synchronize()
     for o, e in zip(outs, grp(x1)):
         assert torch.equal(o, e)
+    # torch.compile: the group op is opaque (fake impl for the list of outputs)
+    f = torch.compile(lambda t: [o * 2.0 for o in grp(t)], fullgraph=True)
+    for o, e in zip(f(x1), grp(x1)):
+        assert torch.equal(o, e * 2.0)
