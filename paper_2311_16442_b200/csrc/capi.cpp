@@ -334,9 +334,9 @@ int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
 }
 
 // batched policy (qweight_b200.h): K4 from QW_GEMM_MIN_BATCH columns up, the
-// batch-1 kernel over the columns (8 to a launch) below -- up to 6 columns
-// one column launch beats K4's fixed cost on q/gate/up, up to 5 on down
-// (profiles/r02_batch_sweep_simt.jsonl)
+// batch-1 kernel over the columns (8 to a launch) below -- up to 5 columns
+// one column launch beats K4 on every 7B shape; at 6 columns K4 wins on
+// down_proj, ties on gate/up and loses on q_proj (profiles/r02_batch_sweep_simt.jsonl)
 bool uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
   static const uint32_t forced = qwdev::knob("QW_GEMM_MIN_BATCH", 0);
   if (batch < 2 || !L->dev.gemm.ok || (flags & QW_LAUNCH_FORCE_COLUMNS)) return false;

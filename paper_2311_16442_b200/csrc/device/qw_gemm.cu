@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (threadIdx.x == 0) {
     for (uint32_t i = 0; i < kWSlots; ++i) mbar_init(&wfull[i], 1), mbar_init(&wempty[i], kDqWarps);
     for (uint32_t i = 0; i < kBSlots; ++i) mbar_init(&bfull[i], 1), mbar_init(&bempty[i], 1);
-    for (uint32_t i = 0; i < kABufs; ++i) mbar_init(&afull[i], kDqWarps), mbar_init(&aempty[i], 1);
+    for (uint32_t i = 0; i < kABufs; ++i) mbar_init(&afull[i], kDqWarps / 2), mbar_init(&aempty[i], 1);
     mbar_init(dfull, 1);
     mbar_fence_init();
   }
@@ -376,11 +376,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           smem_addr(dfull)));
     }
   } else {
-    // ---------------- dequant warps: item = (quad q, group j, channel half h) of a sub-stage.
-    // Lane = quad; warps 2..13 take the 2-bit groups (j < 6), 14..17 the 4-bit
-    // ones, so no warp diverges over the two decode paths.
+    // ---------------- dequant warps: item = (quad q, group j) of a sub-stage, both
+    // 8-channel halves (the per-(row pair, group) constants are formed once
+    // for 16 channels).  Lane = quad; 8 warps per sub-stage, the two warp
+    // halves take alternate sub-stages (two A buffers in flight); warps with
+    // j < 6 take the 2-bit groups, j >= 6 the 4-bit ones, so no warp diverges
+    // over the two decode paths.
     const uint32_t dw = warp - 2, q = lane;
-    const uint32_t j = dw < 12 ? dw >> 1 : 6 + ((dw - 12) >> 1), h = dw & 1u;
+    const uint32_t j = dw & 7u, par = dw >> 3;
     // the quad's row block relative to its tile's first, per segment
     auto rbl_of = [&](uint32_t t) {
       const uint32_t row0 = min((t * kTileQuads + q) * 4, G.rows - 1);
@@ -394,14 +397,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     // (1024 + field) 2^eshl - 1024 2^eshl = eff, exactly (fp16 integers <= 2078 are even above 2048)
     const half2 e2h = __float2half2_rn(eshl ? 2.0f : 1.0f), eoff = __float2half2_rn(eshl ? -2048.0f : -1024.0f);
     const half2 h1024 = __float2half2_rn(1024.0f);
-    const uint32_t a_item = (q & 1u) * 8 + (q >> 1) * kASbo + (2 * j + h) * kALbo;  // + (c % 8) * 16
-    for (uint32_t i = 0; i < nsub; ++i) {
+    const uint32_t a_item = (q & 1u) * 8 + (q >> 1) * kASbo + (2 * j) * kALbo;  // + h kALbo + (c % 8) * 16
+    for (uint32_t i = par; i < nsub; i += 2) {
       const uint32_t wi = i / kSubPerW, s4i = i % kSubPerW, ws = wi % kWSlots, ab = i % kABufs;
-      if (s4i == 0) mbar_wait(&wfull[ws], (wi / kWSlots) & 1u);
-      if (threadIdx.x == 64 && i == 3) gstamp(a, 1);  // sub-stage 3 weights present
+      if (s4i == par) mbar_wait(&wfull[ws], (wi / kWSlots) & 1u);  // this warp's first sub-stage of the stage
+      if (threadIdx.x == 64 && i == 2) gstamp(a, 1);  // sub-stage 2 weights present
       const uint8_t* w = sW + ws * kWStageBytes;
       const uint32_t rb_local = (!kStream || wi < nw0) ? rbl0 : rbl1;
-      uint32_t out[8][2];
+      uint32_t out[2][8][2];  // [half][channel pair][row pair]
       if (j < 6) {
         const uint32_t g6 = 6 * s4i + j;  // 2-bit group within the weight stage
         const uint32_t sc = *reinterpret_cast<const uint32_t*>(w + kOffSo + (rb_local * kSoBoxG + g6) * 4);
@@ -409,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const uint2 m = *reinterpret_cast<const uint2*>(w + kOffMeta + q * kBoxMeta * 4 + 8 * (g6 / 3));
         const half2 Sh = __float2half2_rn(half_bits_to_float(sc) * s2sc);  // scale2 2^(12-P)
         const half2 z2h = __float2half2_rn((float)(sc >> 16));                // zero2 (exact)
-        const uint32_t mm[2] = {m.x, m.y}, cw[2] = {h ? c.y : c.x, h ? c.w : c.z};
+        const uint32_t mm[2] = {m.x, m.y}, cw[2][2] = {{c.x, c.z}, {c.y, c.w}};  // [half][row pair]
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
           const uint32_t v = mm[p];
@@ -425,20 +428,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           M[3] = __hmul2(mrow, __float2half2_rn(64.0f));
           const half2 Z = __hmul2(zh, __hmul2(mrow, __float2half2_rn(-1.0f / 4096.0f)));  // -z mrow 2^-12
 #pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            const uint32_t src = cc < 4 ? cw[p] : cw[p] >> 8;
-            const int b = cc & 3;
-            const half2 t = as_h2(src & (0x00030003u << (2 * b)));
-            out[cc][p] = h2u(__hmul2(__hfma2(t, M[b], Z), Sh));
-          }
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+              const uint32_t src = cc < 4 ? cw[h][p] : cw[h][p] >> 8;
+              const int b = cc & 3;
+              const half2 t = as_h2(src & (0x00030003u << (2 * b)));
+              out[h][cc][p] = h2u(__hmul2(__hfma2(t, M[b], Z), Sh));
+            }
         }
       } else {
         const uint32_t b2 = 2 * s4i + (j - 6);  // 4-bit block within the weight stage
-        const uint2 ca = *reinterpret_cast<const uint2*>(w + kOffC4 + q * kBoxC4 * 4 + 32 * b2 + 8 * h);
-        const uint2 cb = *reinterpret_cast<const uint2*>(w + kOffC4 + q * kBoxC4 * 4 + 32 * b2 + 16 + 8 * h);
+        const uint4 ca = *reinterpret_cast<const uint4*>(w + kOffC4 + q * kBoxC4 * 4 + 32 * b2);
+        const uint4 cb = *reinterpret_cast<const uint4*>(w + kOffC4 + q * kBoxC4 * 4 + 32 * b2 + 16);
         const uint2 s4 = *reinterpret_cast<const uint2*>(w + kOffS4 + q * kBoxS4 * 4 + 8 * b2);
         const uint32_t z4 = *reinterpret_cast<const uint16_t*>(w + kOffZ4 + q * kBoxZ4 * 4 + 2 * b2);
-        const uint32_t cw[2][2] = {{ca.x, ca.y}, {cb.x, cb.y}};
+        // [half][row pair][word]: half h is words (2h, 2h + 1) of each 16-byte code group
+        const uint32_t cw[2][2][2] = {{{ca.x, ca.y}, {cb.x, cb.y}}, {{ca.z, ca.w}, {cb.z, cb.w}}};
         const uint32_t sw[2] = {s4.x, s4.y};
         const half2 M0 = __float2half2_rn(32768.0f), M1 = __float2half2_rn(2048.0f);  // 2^(15-b)
 #pragma unroll
@@ -449,16 +455,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                                   __float2half2_rn(-1.0f / 512.0f));
           const half2 Sh = as_h2(pack_h2(half_bits_to_float(sw[p]) * s4sc, half_bits_to_float(sw[p] >> 16) * s4sc));
 #pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            const uint32_t word = cw[p][cc >> 2];
-            const int nib = cc & 3;
-            const uint32_t src = nib < 2 ? word : word >> 8;
-            const half2 t = as_h2(src & (0x000F000Fu << (4 * (nib & 1))));
-            out[cc][p] = h2u(__hmul2(__hfma2(t, (nib & 1) ? M1 : M0, Z), Sh));
-          }
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+              const uint32_t word = cw[h][p][cc >> 2];
+              const int nib = cc & 3;
+              const uint32_t src = nib < 2 ? word : word >> 8;
+              const half2 t = as_h2(src & (0x000F000Fu << (4 * (nib & 1))));
+              out[h][cc][p] = h2u(__hmul2(__hfma2(t, (nib & 1) ? M1 : M0, Z), Sh));
+            }
         }
       }
-      if (s4i + 1 == kSubPerW || i + 1 == nsub) {  // last use of this weight slot
+      if (s4i + 2 >= kSubPerW || i + 2 >= nsub) {  // this warp's last use of the weight slot
         __syncwarp();
         if (lane == 0) mbar_arrive(&wempty[ws]);
       }
@@ -467,12 +475,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
       uint8_t* at = sA + ab * kATileBytes + a_item;
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc)
-        *reinterpret_cast<uint2*>(at + cc * 16) = make_uint2(out[cc][0], out[cc][1]);
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<uint2*>(at + h * kALbo + cc * 16) = make_uint2(out[h][cc][0], out[h][cc][1]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&afull[ab]);
-
     }
     // ---------------- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
     if (warp < 6) {

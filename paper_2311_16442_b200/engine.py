@@ -151,7 +151,7 @@ class DeviceLayer:
             raise QWeightError(1, "matvec: out must be a contiguous cuda float32 tensor of batch * rows "
                                   "elements on the activation's device")
         ws = workspace or default_workspace(self.device)
-        # batched: "auto" (K4 from 7 columns, the batch-1 kernel over the
+        # batched: "auto" (K4 from 6 columns, the batch-1 kernel over the
         # columns below), "gemm" (force the tcgen05 GEMM K4), "columns"
         # (force the batch-1 kernel, up to 8 columns per launch)
         flags = (1 if pdl else 0) | (2 if x_independent else 0) | {"auto": 0, "gemm": 4, "columns": 8}[batched]
