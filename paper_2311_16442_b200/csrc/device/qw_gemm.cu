@@ -330,10 +330,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         tma_load_2d(dst + kOffZ4, &a.tm[4], (int)(G.off_z4 / 4 + 4 * wst), qy, &wfull[ws]);
         tma_load_2d(dst + kOffSo, &a.tso, (int)(24 * wst), (int)rb_of(t), &wfull[ws]);
       };
-      const uint32_t wpre = min(nw, kWSlots);
-      for (uint32_t i = 0; i < wpre; ++i) load_w(i);  // the weights do not depend on x
-      pdl_wait();  // B tiles are the prologue kernel's output
-      uint32_t wnext = wpre;
+      // the weights do not depend on x; a weight slot is refilled once every
+      // dequant warp left it
+      for (uint32_t i = 0; i < nw; ++i) load_w(i);
+    } else if (lane == 1) {
+      // B tiles (the prologue kernel's output) from their own thread: a B
+      // refill must not wait behind a weight-slot refill (the MMA would
+      // starve, the A buffers fill up and the dequant warps stall)
+      pdl_wait();
       for (uint32_t i = 0; i < nsub; ++i) {
         const uint32_t bs = i % kBSlots;
         if (i >= kBSlots) mbar_wait(&bempty[bs], ((i / kBSlots) - 1) & 1u);
@@ -341,9 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const uint32_t u = wst_of(i / kSubPerW) * kSubPerW + i % kSubPerW;  // sub-stage within the tile's K
         bulk_load_nohint(sB + bs * kBStageBytes, a.xpt + (size_t)u * (kBStageBytes / 2), kBStageBytes,
                          &bfull[bs]);
-        if ((i % kSubPerW) == 0 && wnext < nw) load_w(wnext++);
       }
-      while (wnext < nw) load_w(wnext++);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
