@@ -434,9 +434,14 @@ int upload_packed(const qwb::PackedLayer& L, int device, uint32_t flags, qw_laye
     }
     qwdev::mma_geometry(H->dev.mg, H->dev.g);
     // batch-1 kernel policy (header): auto picks K2m where K2's plan falls
-    // back to the global-memory CSR loop or exceeds two groups per lane
+    // back to its global-memory CSR loop with more than ~1.5 K outliers per
+    // CTA (13B down_proj: K2 12.5 / 13.5 us vs K2m 15.6 at 0.1 / 0.2 %, but
+    // 25.1 / 46.0 vs 15.8 / 16.5 at 0.5 / 1 %), needs more than two groups
+    // per lane outside the wide layout, or cannot stage x (> 16384 columns)
     const auto& gp = H->dev.plan;
-    const bool k2_slow = (L.csr.nnz() > 0 && !gp.csr_stage) || (gp.kmax > 2 && !gp.wide) || !gp.xsm;
+    uint32_t ent_max = 0;
+    for (uint32_t c = 0; c < gp.grid; ++c) ent_max = std::max(ent_max, gp.cta_e1[c] - gp.cta_e0[c]);
+    const bool k2_slow = (L.csr.nnz() > 0 && !gp.csr_stage && ent_max > 1536) || (gp.kmax > 2 && !gp.wide) || !gp.xsm;
     const bool want_mma = (flags & QW_UPLOAD_TENSOR_CORE) || (!(flags & QW_UPLOAD_SIMT) && k2_slow);
     if (H->dev.mg.ok && want_mma) {
       std::vector<uint8_t> recs;

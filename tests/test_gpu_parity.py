@@ -454,11 +454,14 @@ def test_linear_stack_run_end_to_end():
 
 def test_auto_kernel_policy():
     """kernel="auto": K2 (SIMT) where it measured faster, K2m (warp MMA) for
-    outliers that overflow K2's CSR stage and for layers wider than 16384."""
+    outliers that overflow K2's CSR stage and for layers wider than 16384
+    (13B down_proj: K2m at 1 % outliers, K2 at 0.1 %)."""
     dense = qw.synth_layer(5120, 13824, seed=3, outlier_ratio=0.01)  # Llama-2-13B down_proj, 1 %
+    sparse = qw.synth_layer(5120, 13824, seed=3, outlier_ratio=0.001)  # the same shape at 0.1 %: K2 fits
     wide = qw.synth_layer(64, 28672, seed=4)
     plain = qw.synth_layer(256, 4096, seed=5)
     assert qw.DeviceLayer(dense).uses_tensor_core
+    assert not qw.DeviceLayer(sparse).uses_tensor_core
     assert qw.DeviceLayer(wide).uses_tensor_core
     assert not qw.DeviceLayer(plain).uses_tensor_core
     assert not qw.DeviceLayer(dense, kernel="simt").uses_tensor_core
