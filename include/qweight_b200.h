@@ -232,6 +232,12 @@ int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out);
 int qw_group_free(qw_group* group);
 int qw_group_matvec(const qw_group* group, const float* x, float* const* ys, void* stream,
                     uint32_t flags);
+/* Batched group launch: x device fp32 [batch][cols], ys[i] device fp32
+ * [batch][rows_i]; up to 8 / n columns of every layer share one launch (one
+ * segment per (layer, column), the layers' weights read once per launch and
+ * shared through L2), each output bit-identical to the layer's batch-1 call. */
+int qw_group_matvec_batch(const qw_group* group, const float* x, uint32_t batch, float* const* ys,
+                          void* stream, uint32_t flags);
 /* Decode chains: while a launch of `layer` (or `group`) runs, its CTAs also
  * stream the packed weights of `next` (the layers of the launch that follows
  * on the stream) from HBM into L2, so HBM keeps streaming while the SMs finish

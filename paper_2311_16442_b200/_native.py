@@ -97,6 +97,8 @@ _SIGS = {
     "qw_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32, C.POINTER(C.c_void_p)]),
     "qw_group_free": (C.c_int, [C.c_void_p]),
     "qw_group_matvec": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p, C.c_uint32]),
+    "qw_group_matvec_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p), C.c_void_p,
+                                        C.c_uint32]),
     "qw_layer_set_prefetch": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_uint32]),
     "qw_chain_create": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "qw_chain_run": (C.c_int, [C.c_void_p, C.c_void_p]),

@@ -53,6 +53,10 @@ struct qw_group {
   bool mma = false;  // every layer has the tensor-core tile format
   std::vector<const qwdev::DeviceLayer*> layers;  // borrowed
   int device = 0;
+  // batches: c columns of every layer in one launch (n * c <= kMaxSeg
+  // segments, layer-major); index c, grid 0 = not planned
+  std::vector<qwdev::GemvPlan> cplans;
+  std::vector<qwdev::MmaPlan> mcplans;
 };
 
 struct qw_chain {
@@ -923,6 +927,20 @@ int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out) {
       if (int me = qwdev::plan_mma(G->mplan, G->layers.data(), rps.data(), n, layers[0]->num_sms))
         return cuda_fail((cudaError_t)me, "group mma plan");
     }
+    // batched group launches: c columns x n layers as one grid
+    const uint32_t cmax = qwdev::kMaxSeg / n;
+    G->cplans.assign(cmax + 1, qwdev::GemvPlan{});
+    G->mcplans.assign(cmax + 1, qwdev::MmaPlan{});
+    for (uint32_t c = 2; c <= cmax; ++c) {
+      std::vector<const qwdev::DeviceLayer*> lay;
+      std::vector<const uint32_t*> rp;
+      for (uint32_t i = 0; i < n; ++i)
+        for (uint32_t k = 0; k < c; ++k) lay.push_back(G->layers[i]), rp.push_back(rps[i]);
+      if (qwdev::plan_gemv_group(G->cplans[c], lay.data(), rp.data(), n * c, layers[0]->num_sms))
+        G->cplans[c] = qwdev::GemvPlan{}, G->cplans[c].grid = 0;
+      if (G->mma && qwdev::plan_mma(G->mcplans[c], lay.data(), rp.data(), n * c, layers[0]->num_sms))
+        G->mcplans[c] = qwdev::MmaPlan{}, G->mcplans[c].grid = 0;
+    }
     *out = G.release();
     return (int)QW_OK;
   });
@@ -930,6 +948,46 @@ int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out) {
 
 int qw_group_free(qw_group* g) {
   delete g;
+  return QW_OK;
+}
+
+int qw_group_matvec_batch(const qw_group* g, const float* x, uint32_t batch, float* const* ys, void* stream,
+                          uint32_t flags) {
+  if (!g || !x || !ys) return fail(QW_ERR_ARG, "group matvec: null argument");
+  if (batch == 0 || batch > 16) return fail(QW_ERR_ARG, "group matvec: batch must be in 1..16");
+  const uint32_t n = (uint32_t)g->layers.size();
+  for (uint32_t i = 0; i < n; ++i)
+    if (!ys[i]) return fail(QW_ERR_ARG, "group matvec: null output");
+  int dev_now = -1;
+  cudaGetDevice(&dev_now);
+  if (dev_now != g->device) cudaSetDevice(g->device);
+  const uint32_t xflags = (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u;
+  const bool pdl = (flags & QW_LAUNCH_PDL) != 0;
+  const uint32_t cols = g->layers[0]->g.cols, cmax = std::max<uint32_t>(1, qwdev::kMaxSeg / n);
+  for (uint32_t c0 = 0; c0 < batch;) {
+    uint32_t cb = std::min(cmax, batch - c0);
+    const bool planned = cb > 1 && (g->mma ? g->mcplans[cb].grid : g->cplans[cb].grid) != 0;
+    if (!planned) cb = 1;
+    const qwdev::DeviceLayer* lay[qwdev::kMaxSeg];
+    const float* xs[qwdev::kMaxSeg];
+    float* yo[qwdev::kMaxSeg];
+    uint32_t slot[qwdev::kMaxSeg];
+    uint32_t s = 0;
+    for (uint32_t i = 0; i < n; ++i)  // layer-major segments, as planned
+      for (uint32_t k = 0; k < cb; ++k, ++s) {
+        lay[s] = g->layers[i], slot[s] = k;
+        xs[s] = x + (size_t)(c0 + k) * cols;
+        yo[s] = ys[i] + (size_t)(c0 + k) * g->layers[i]->g.rows;
+      }
+    int e;
+    if (g->mma)
+      e = qwdev::launch_mma(cb > 1 ? g->mcplans[cb] : g->mplan, lay, s, xs, yo, stream, pdl, xflags, slot);
+    else
+      e = qwdev::launch_gemv_group(cb > 1 ? g->cplans[cb] : g->plan, lay, s, xs, yo, stream, pdl, xflags, nullptr,
+                                   1, false);
+    if (e) return cuda_fail((cudaError_t)e, "group launch");
+    c0 += cb;
+  }
   return QW_OK;
 }
 
@@ -1061,7 +1119,7 @@ int qw_debug_group_timeline(const qw_group* g, const float* x, float* const* ys,
   std::fill(xs, xs + qwdev::kMaxSeg, x);
   // K2m groups: %globaltimer stamps at the K2m events (qw_mma.cu)
   const int e = g->mma ? qwdev::launch_mma(g->mplan, g->layers.data(), (uint32_t)g->layers.size(), xs, ys, stream,
-                                           flags & 1u, (flags & 4u) ? qwdev::kXIndependent : 0u, false, stamps)
+                                           flags & 1u, (flags & 4u) ? qwdev::kXIndependent : 0u, nullptr, stamps)
                        : qwdev::launch_gemv_group(g->plan, g->layers.data(), (uint32_t)g->layers.size(), xs, ys,
                                                   stream, flags & 1u, (flags & 4u) ? qwdev::kXIndependent : 0u,
                                                   stamps, 1, (flags & 2u) != 0);

@@ -46,9 +46,11 @@ int launch_columns(const DeviceLayer& L, const float* x, uint32_t batch, float* 
       const MmaPlan* p = n == 1 ? &L.mplan : &L.mcplan[n - 2];
       if (n > 1 && p->grid == 0) {  // no column plan: one launch per column
         for (uint32_t s = 0; s < n && !e; ++s)
-          e = launch_mma(L.mplan, same, 1, xs + s, ys + s, stream, pdl, flags, false);
+          e = launch_mma(L.mplan, same, 1, xs + s, ys + s, stream, pdl, flags, nullptr);
       } else {
-        e = launch_mma(*p, same, n, xs, ys, stream, pdl, flags, true);
+        uint32_t slots[kMaxSeg];
+        for (uint32_t s = 0; s < kMaxSeg; ++s) slots[s] = s;
+        e = launch_mma(*p, same, n, xs, ys, stream, pdl, flags, slots);
       }
     } else {
       const GemvPlan* p = n == 1 ? &L.plan : &L.cplan[n - 2];

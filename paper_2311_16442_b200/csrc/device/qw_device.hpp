@@ -218,9 +218,10 @@ int plan_mma(MmaPlan& p, const DeviceLayer* const* layers, const uint32_t* const
              int num_sms);
 int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* x,
                float* const* ys, void* stream, bool pdl, uint32_t flags);
-// segment s reads xs[s]; column_slots: segment s uses the layer's scratch slot s
+// segment s reads xs[s]; slots (or null: slot 0): segment s uses its layer's
+// chunk-partial scratch slot slots[s] (< kMaxSeg; distinct for the columns of one layer)
 int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
-               float* const* ys, void* stream, bool pdl, uint32_t flags, bool column_slots,
+               float* const* ys, void* stream, bool pdl, uint32_t flags, const uint32_t* slots,
                unsigned long long* dbg = nullptr);
 
 // Decode chain (batch 1): a sequence of launch steps (each a group of 1..4

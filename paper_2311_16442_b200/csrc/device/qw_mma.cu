@@ -1061,7 +1061,7 @@ int plan_mma(MmaPlan& p, const DeviceLayer* const* layers, const uint32_t* const
 }
 
 int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
-               float* const* ys, void* stream, bool pdl, uint32_t flags, bool column_slots,
+               float* const* ys, void* stream, bool pdl, uint32_t flags, const uint32_t* slots,
                unsigned long long* dbg) {
   const DeviceLayer& L0 = *layers[0];
   const MmaGeometry& m = L0.mg;
@@ -1075,7 +1075,7 @@ int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, c
     a.y[l] = ys[s];
     a.xs[l] = xs[s];
     // the columns of one layer must not share its chunk-partial scratch
-    const uint32_t slot = column_slots ? s : 0u;
+    const uint32_t slot = slots ? slots[s] : 0u;
     a.part[l] = L.mpart ? L.mpart + slot * part_slot : nullptr;
     a.cnt[l] = L.mcnt ? L.mcnt + slot * m.RT : nullptr;
     a.rows[l] = L.g.rows, a.RT[l] = L.mg.RT;
@@ -1100,7 +1100,7 @@ int launch_mma(const MmaPlan& p, const DeviceLayer* const* layers, uint32_t n, c
                float* const* ys, void* stream, bool pdl, uint32_t flags) {
   const float* xs[kMaxSeg];
   std::fill(xs, xs + kMaxSeg, x);
-  return launch_mma(p, layers, n, xs, ys, stream, pdl, flags, false, nullptr);
+  return launch_mma(p, layers, n, xs, ys, stream, pdl, flags, nullptr, nullptr);
 }
 
 // ------------------------------------------------------------ decode chain

@@ -328,15 +328,28 @@ class LayerGroup:
         check(lib().qw_group_set_prefetch(self._h, _handles(next_layers), len(next_layers)))
 
     def matvec(self, x, outs=None, stream=None, pdl: bool = False, x_independent: bool = False):
-        """x: cuda fp32 [cols] (original order); returns one [rows] output per layer."""
-        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous() or x.dim() != 1:
-            raise QWeightError(1, "group matvec: x must be a contiguous 1-D cuda float32 tensor")
-        if x.shape[0] != self.layers[0].cols:
+        """x: cuda fp32 [cols] or [batch, cols] (original order); returns one
+        [rows] / [batch, rows] output per layer.  A batch runs up to 8 / n
+        columns of every layer per launch (qw_group_matvec_batch)."""
+        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous() or x.dim() not in (1, 2):
+            raise QWeightError(1, "group matvec: x must be a contiguous 1-D or 2-D cuda float32 tensor")
+        if x.shape[-1] != self.layers[0].cols:
             raise QWeightError(1, "group matvec: activation length != input channels")
+        batch = 1 if x.dim() == 1 else x.shape[0]
+        shape = (lambda r: (r,)) if x.dim() == 1 else (lambda r: (batch, r))
         if outs is None:
-            outs = [torch.empty(d.rows, dtype=torch.float32, device=x.device) for d in self.layers]
+            outs = [torch.empty(shape(d.rows), dtype=torch.float32, device=x.device) for d in self.layers]
+        for o, d in zip(outs, self.layers):
+            if (o.dtype != torch.float32 or not o.is_cuda or not o.is_contiguous() or o.numel() != batch * d.rows
+                    or o.device != x.device):
+                raise QWeightError(1, "group matvec: every output must be a contiguous cuda float32 tensor of "
+                                      "batch * rows elements on the activation's device")
         ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
         flags = (1 if pdl else 0) | (2 if x_independent else 0)
-        check(lib().qw_group_matvec(self._h, C.c_void_p(x.data_ptr()), ptrs,
-                                    C.c_void_p(_stream_handle(stream)), flags))
+        if x.dim() == 1:
+            check(lib().qw_group_matvec(self._h, C.c_void_p(x.data_ptr()), ptrs,
+                                        C.c_void_p(_stream_handle(stream)), flags))
+        else:
+            check(lib().qw_group_matvec_batch(self._h, C.c_void_p(x.data_ptr()), batch, ptrs,
+                                              C.c_void_p(_stream_handle(stream)), flags))
         return outs

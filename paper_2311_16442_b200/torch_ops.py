@@ -49,15 +49,19 @@ def _(x: torch.Tensor, layer_id: int) -> torch.Tensor:
 
 @torch.library.custom_op("qweight_b200::quantized_linear_group", mutates_args=())
 def quantized_linear_group(x: torch.Tensor, group_id: int) -> list[torch.Tensor]:
-    """[W_i x for each layer of the registered group]: batch 1 is ONE fused
-    launch for all the layers (q/k/v, gate/up: one dependency wait, one
-    activation staging); larger batches run each layer's batched path."""
+    """[W_i x for each layer of the registered group]: one fused launch for all
+    the layers (q/k/v, gate/up: one dependency wait, one activation staging)
+    per up to 8 / n columns while the batched policy keeps the batch-1
+    kernel; larger batches run each layer's K4 GEMM."""
     grp = _GROUPS[group_id]
     lead = x.shape[:-1]
     xb = x.reshape(-1, x.shape[-1]).contiguous()
     if xb.shape[0] == 1:
         return [y.reshape(*lead, y.shape[0]) for y in grp.matvec(xb.reshape(-1), pdl=True)]
-    return [quantized_linear(x, lid) for lid in grp.layer_ids]
+    if all(_REGISTRY[lid].batched_path(xb.shape[0]) == "columns" for lid in grp.layer_ids):
+        # the batch-1 kernel: up to 8 / n columns of every layer per launch
+        return [y.reshape(*lead, y.shape[-1]) for y in grp.matvec(xb, pdl=True)]
+    return [quantized_linear(x, lid) for lid in grp.layer_ids]  # each layer's K4 GEMM
 
 
 @quantized_linear_group.register_fake
