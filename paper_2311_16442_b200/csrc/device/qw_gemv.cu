@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     const float4* gx = reinterpret_cast<const float4*>(g_x);
     float4* sx4 = reinterpret_cast<float4*>(s_x);
     const uint32_t n4 = G.cols >> 2;
-    constexpr int kXr = 4;
+    constexpr int kXr = KG >= 2 ? 5 : 4;  // 5 x 16 B x 576 threads: 11008 channels in one round trip
     float4 xr[kXr];
     auto x_issue = [&]() {
       if (a.wait_x) pdl_wait();
