@@ -1151,7 +1151,7 @@ int qw_launches_per_matvec(const qw_layer* L, uint32_t batch) {
 }
 
 int qw_matvec_uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
-  if (!L) return fail(QW_ERR_ARG, "uses_gemm: null layer");
+  if (!L) return -fail(QW_ERR_ARG, "uses_gemm: null layer");  // negative: 0 / 1 are answers
   return uses_gemm(L, batch, flags) ? 1 : 0;
 }
 

@@ -238,7 +238,7 @@ class DeviceLayer:
         the columns, up to 8 per launch) for a matvec of `batch` columns."""
         r = lib().qw_matvec_uses_gemm(self._h, batch, {"auto": 0, "gemm": 4, "columns": 8}[batched])
         if r < 0:
-            check(r)
+            check(-r)
         return "gemm" if r else "columns"
 
 

@@ -54,6 +54,19 @@ def test_abi_version_and_strerror():
     assert L.qw_strerror(99) == b"unknown status"
 
 
+def test_null_handles_are_argument_errors_without_a_device():
+    """The ABI never dereferences a null handle: every entry that takes one
+    returns QW_ERR_ARG (status 1) before touching CUDA."""
+    import ctypes as C
+    L = qw.lib()
+    null = C.c_void_p()
+    outs = (C.c_void_p * 1)()
+    assert L.qw_group_matvec(null, null, outs, null, 0) == 1
+    assert L.qw_group_matvec_batch(null, null, 2, outs, null, 0) == 1
+    assert L.qw_matvec_uses_gemm(null, 4, 0) == -1  # (0 / 1 are answers)
+    assert L.qw_matvec_ex(null, null, 1, null, null, null, 0) == 1
+
+
 def test_invalid_view_is_rejected_with_layer_status():
     import dataclasses
     layer = qw.synth_layer(8, 64, seed=1)
