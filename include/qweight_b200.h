@@ -326,6 +326,26 @@ int qw_debug_gemm_timeline(const qw_layer* layer, const float* x, uint32_t batch
 /* Number of kernels one qw_matvec call launches. */
 int qw_launches_per_matvec(const qw_layer* layer, uint32_t batch);
 int qw_launches_per_matvec_ex(const qw_layer* layer, uint32_t batch, uint32_t flags);
+/* Tensor parallel over peer memory (the collective fused with
+ * the GEMV; NVLink P2P between GPUs, CUDA IPC mappings between processes).
+ * qw_matvec_push: y = W_q x (batch 1, the SIMT kernel: upload with
+ * QW_UPLOAD_SIMT) and the kernel's epilogue also stores the rows into
+ * peer_y[i] (the caller offsets each pointer to where this rank's rows go),
+ * then every CTA adds 1 to *peer_flag[i] (system scope, after a release).
+ * qw_push_arrivals: the arrivals one push adds to each peer's counter (its
+ * grid).  qw_peer_wait: stream-ordered wait until *flag >= expected (the
+ * sum of the ranks' arrivals), which then takes `expected` off the counter
+ * (no reset needed; CUDA-graph capturable).  qw_peer_reduce: y[i] =
+ * sum_r staging[r * n + i] in rank order (the row split's partial sums).
+ * qw_ipc_*: 64-byte CUDA IPC handles of device buffers for the exchange. */
+int qw_matvec_push(const qw_layer* layer, const float* x, float* y, float* const* peer_y,
+                   uint32_t* const* peer_flag, uint32_t npeer, void* stream, uint32_t flags);
+int qw_push_arrivals(const qw_layer* layer);
+int qw_peer_wait(uint32_t* flag, uint32_t expected, void* stream);
+int qw_peer_reduce(const float* staging, uint32_t world, uint32_t n, float* y, void* stream);
+int qw_ipc_handle(const void* dev_ptr, uint8_t handle[64]);
+int qw_ipc_open(const uint8_t handle[64], void** dev_ptr);
+int qw_ipc_close(void* dev_ptr);
 /* 1 if a qw_matvec_ex call of `batch` columns with `flags` runs the tcgen05
  * GEMM K4, 0 if it runs the batch-1 kernel over the columns; < 0 on error. */
 int qw_matvec_uses_gemm(const qw_layer* layer, uint32_t batch, uint32_t flags);

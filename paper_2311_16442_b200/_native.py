@@ -125,6 +125,14 @@ _SIGS = {
                                          C.c_void_p]),
     "qw_launches_per_matvec": (C.c_int, [C.c_void_p, C.c_uint32]),
     "qw_launches_per_matvec_ex": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32]),
+    "qw_matvec_push": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p),
+                                 C.POINTER(C.c_void_p), C.c_uint32, C.c_void_p, C.c_uint32]),
+    "qw_push_arrivals": (C.c_int, [C.c_void_p]),
+    "qw_peer_wait": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "qw_peer_reduce": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "qw_ipc_handle": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "qw_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "qw_ipc_close": (C.c_int, [C.c_void_p]),
     "qw_matvec_uses_gemm": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32]),
     "qw_debug_gemm_shift": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     "qw_debug_knob": (C.c_uint32, [C.c_char_p, C.c_uint32]),

@@ -1150,6 +1150,70 @@ int qw_launches_per_matvec(const qw_layer* L, uint32_t batch) {
   return qw_launches_per_matvec_ex(L, batch, 0u);
 }
 
+int qw_matvec_push(const qw_layer* L, const float* x, float* y, float* const* peer_y, uint32_t* const* peer_flag,
+                   uint32_t npeer, void* stream, uint32_t flags) {
+  if (!L || !x || !y || (npeer && (!peer_y || !peer_flag))) return fail(QW_ERR_ARG, "push: null argument");
+  if (npeer > qwdev::kMaxPeer) return fail(QW_ERR_ARG, "push: at most 8 peers");
+  if (L->dev.mrecs) return fail(QW_ERR_UNSUPPORTED, "push: the fused exchange runs on the SIMT kernel (upload with QW_UPLOAD_SIMT)");
+  qwdev::PeerOut po{};
+  for (uint32_t i = 0; i < npeer; ++i) {
+    if (!peer_y[i] || !peer_flag[i]) return fail(QW_ERR_ARG, "push: null peer buffer");
+    po.y[i] = peer_y[i], po.flag[i] = peer_flag[i];
+  }
+  po.n = npeer;
+  int dev_now = -1;
+  cudaGetDevice(&dev_now);
+  if (dev_now != L->device) cudaSetDevice(L->device);
+  const qwdev::DeviceLayer* one[1] = {&L->dev};
+  const float* xs[1] = {x};
+  float* ys[1] = {y};
+  const uint32_t xflags = (flags & QW_LAUNCH_X_INDEPENDENT) ? qwdev::kXIndependent : 0u;
+  const int e = qwdev::launch_gemv_group(L->dev.plan, one, 1, xs, ys, stream, (flags & QW_LAUNCH_PDL) != 0, xflags,
+                                         nullptr, 1, false, &po);
+  return e ? cuda_fail((cudaError_t)e, "push launch") : QW_OK;
+}
+
+int qw_push_arrivals(const qw_layer* L) {
+  if (!L) return -fail(QW_ERR_ARG, "push arrivals: null layer");
+  return (int)L->dev.plan.grid;
+}
+
+int qw_peer_wait(uint32_t* flag, uint32_t expected, void* stream) {
+  if (!flag) return fail(QW_ERR_ARG, "peer wait: null counter");
+  const int e = qwdev::launch_peer_wait(flag, expected, stream);
+  return e ? cuda_fail((cudaError_t)e, "peer wait") : QW_OK;
+}
+
+int qw_peer_reduce(const float* staging, uint32_t world, uint32_t n, float* y, void* stream) {
+  if (!staging || !y || world == 0) return fail(QW_ERR_ARG, "peer reduce: null argument");
+  const int e = qwdev::launch_peer_reduce(staging, world, n, y, stream);
+  return e ? cuda_fail((cudaError_t)e, "peer reduce") : QW_OK;
+}
+
+int qw_ipc_handle(const void* dev_ptr, uint8_t out[64]) {
+  if (!dev_ptr || !out) return fail(QW_ERR_ARG, "ipc handle: null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle size");
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  std::memcpy(out, &h, 64);
+  return QW_OK;
+}
+
+int qw_ipc_open(const uint8_t handle[64], void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(QW_ERR_ARG, "ipc open: null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? QW_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+int qw_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(QW_ERR_ARG, "ipc close: null pointer");
+  const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  return e == cudaSuccess ? QW_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
 int qw_matvec_uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
   if (!L) return -fail(QW_ERR_ARG, "uses_gemm: null layer");  // negative: 0 / 1 are answers
   return uses_gemm(L, batch, flags) ? 1 : 0;

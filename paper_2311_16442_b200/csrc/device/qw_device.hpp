@@ -162,6 +162,17 @@ struct DeviceLayer {
   uint32_t* csr = nullptr;       // nnz (perm[col] | fp16 << 16): x channel + value
 };
 
+// Fused exchange over peer memory (tensor parallel, batch 1): besides its own
+// y, a launch stores its rows into every peer's buffer (NVLink P2P or
+// same-device IPC mappings, offset by the caller) and each CTA then adds 1 to
+// every peer's arrival counter (system scope, after a release fence).
+constexpr uint32_t kMaxPeer = 8;
+struct PeerOut {
+  float* y[kMaxPeer];
+  uint32_t* flag[kMaxPeer];
+  uint32_t n;
+};
+
 // Per-stream scratch (kept in the ABI for the batched path; the fused
 // batch-1 kernel needs none).
 struct Workspace {
@@ -184,7 +195,12 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
                       float* const* ys, void* stream, bool pdl, uint32_t flags);
 int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
                       float* const* ys, void* stream, bool pdl, uint32_t flags, unsigned long long* dbg,
-                      uint32_t repeat, bool global_clock);
+                      uint32_t repeat, bool global_clock, const PeerOut* peers = nullptr);
+// peer-memory exchange kernels (qw_peer.cu): wait until *flag >= expected,
+// then take `expected` off it (arrivals of a later launch stay counted)
+int launch_peer_wait(uint32_t* flag, uint32_t expected, void* stream);
+// y[i] = sum_{r < world} staging[r * n + i] in rank order (a P2P all-reduce's local step)
+int launch_peer_reduce(const float* staging, uint32_t world, uint32_t n, float* y, void* stream);
 // Batch of 2..16 columns on the batch-1 kernel of the layer (K2 or K2m): the
 // columns go kMaxSeg to a launch, one grid split over them like a layer
 // group (each segment its own x and y, the same weights, read once from HBM

@@ -81,6 +81,7 @@ struct GemvArgs {
   uint32_t pf_bytes[GemvPlan::kMaxPf], pf_n, pf_late;
   unsigned long long* dbg;  // optional timeline: kTimelineEvents stamps per CTA
   uint32_t dbg_global;      // stamps from %globaltimer (ns) instead of clock64
+  PeerOut peers;            // fused exchange: y rows also to peer buffers, then arrival counters
   uint8_t cta_seg[kMaxGrid];
   uint32_t cta_q0[kMaxGrid], cta_q1[kMaxGrid], cta_e0[kMaxGrid], cta_e1[kMaxGrid];
 };
@@ -99,12 +100,33 @@ __device__ __forceinline__ void stamp_impl(const GemvArgs& a, uint32_t ev) {
   } while (0)
 
 
+// The fused tensor-parallel exchange (GemvArgs::peers): the CTA's rows, summed
+// exactly as for y, into every peer's buffer; once every consumer's stores
+// are issued, thread 0 makes one cumulative system-scope release and adds
+// the CTA's arrival to every peer's counter (qw_peer.cu waits for them).
+__device__ __forceinline__ void push_peers(const PeerOut& po, const float* s_part, const float* s_csr, uint32_t W,
+                                        uint32_t nrows, uint32_t r_begin, uint32_t nthreads) {
+  for (uint32_t t = threadIdx.x; t < nrows; t += nthreads) {
+    const float* p = s_part + t * W;
+    float s = p[0];
+    for (uint32_t w2 = 1; w2 < W; ++w2) s += p[w2];
+    const float v = s + s_csr[t];
+    for (uint32_t q = 0; q < po.n; ++q) po.y[q][r_begin + t] = v;
+  }
+  named_sync(4, nthreads);
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (uint32_t q = 0; q < po.n; ++q)
+      asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(po.flag[q]) : "memory");
+  }
+}
+
 // KG groups per lane, NQ quads per ring slot (decoded together for ILP),
 // UNI: group2 % 4 == 0 (a quad never straddles 2-order blocks), XSM: x is
 // staged in shared memory (TMA) before the gather.
 // TM: two teams of consumer warps take alternate units (long quad ranges:
 // group launches, wide layers); then the CTA owns the SM (no PDL co-residency).
-template <int KG, int NQ, bool UNI, bool XSM, bool TM = false>
+template <int KG, int NQ, bool UNI, bool XSM, bool TM = false, bool PEER = false>
 __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 2) ? 1 : 2)
     gemv_kernel(const __grid_constant__ GemvArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -698,28 +720,36 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     for (uint32_t w2 = 1; w2 < W; ++w2) s += p[w2];
     g_y[r_begin + t] = s + s_csr[t];
   }
+  // fused TP exchange: a separate instantiation (PEER), so the kernels that
+  // never push keep their code generation
+  if constexpr (PEER) push_peers(a.peers, s_part, s_csr, W, nrows, r_begin, NC * 32);
   if (threadIdx.x == 0) stamp(a.dbg, 5);
 }
 
 using GemvFn = void (*)(GemvArgs);
 
-template <bool UNI, bool XSM>
+template <bool UNI, bool XSM, bool PEER = false>
 GemvFn pick2(uint32_t kg) {
   switch (kg) {
     case 1:
-      if (UNI && env_u32("QW_NQ1", 2) == 2) return gemv_kernel<1, 2, UNI, XSM>;
-      return gemv_kernel<1, UNI ? 4 : 1, UNI, XSM>;
-    case 2: return gemv_kernel<2, UNI ? 2 : 1, UNI, XSM>;
-    case 3: return gemv_kernel<3, 1, UNI, XSM>;
-    default: return gemv_kernel<4, 1, UNI, XSM>;
+      if (UNI && env_u32("QW_NQ1", 2) == 2) return gemv_kernel<1, 2, UNI, XSM, false, PEER>;
+      return gemv_kernel<1, UNI ? 4 : 1, UNI, XSM, false, PEER>;
+    case 2: return gemv_kernel<2, UNI ? 2 : 1, UNI, XSM, false, PEER>;
+    case 3: return gemv_kernel<3, 1, UNI, XSM, false, PEER>;
+    default: return gemv_kernel<4, 1, UNI, XSM, false, PEER>;
   }
 }
+template <bool PEER = false>
 GemvFn pick_teams(uint32_t kg) {
-  return kg == 1 ? gemv_kernel<1, 2, true, true, true> : gemv_kernel<2, 2, true, true, true>;
+  return kg == 1 ? gemv_kernel<1, 2, true, true, true, PEER> : gemv_kernel<2, 2, true, true, true, PEER>;
 }
 GemvFn pick_kernel(uint32_t kg, bool uni, bool xsm) {
   return uni ? (xsm ? pick2<true, true>(kg) : pick2<true, false>(kg))
              : (xsm ? pick2<false, true>(kg) : pick2<false, false>(kg));
+}
+// the exchange variants: group2 % 4 == 0 layers only (every Llama config)
+GemvFn pick_peer(uint32_t kg, bool xsm, bool teams) {
+  return teams ? pick_teams<true>(kg) : (xsm ? pick2<true, true, true>(kg) : pick2<true, false, true>(kg));
 }
 uint32_t quads_per_slot(uint32_t kg, bool uni) {
   return !uni ? 1u : (kg == 1 ? env_u32("QW_NQ1", 2) : (kg == 2 ? 2u : 1u));
@@ -921,6 +951,14 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
                                              (int)(227 * 1024));
       if (err != cudaSuccess) return (int)err;
     }
+    for (bool teams : {false, true})
+      for (bool xsm : {false, true})
+        for (uint32_t k : {1u, 2u, 3u, 4u}) {
+          if (teams && (!xsm || k > 2)) continue;
+          cudaError_t err = cudaFuncSetAttribute(pick_peer(k, xsm, teams), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)(227 * 1024));
+          if (err != cudaSuccess) return (int)err;
+        }
     if (cur < 64) attr_dev |= 1ull << cur;
   }
   return 0;
@@ -955,7 +993,7 @@ int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_
 
 int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,
                       float* const* ys, void* stream, bool pdl, uint32_t flags, unsigned long long* dbg,
-                      uint32_t repeat, bool global_clock) {
+                      uint32_t repeat, bool global_clock, const PeerOut* peers) {
   const Geometry& G = layers[0]->g;
   GemvArgs a;
   for (uint32_t l = 0; l < kMaxSeg; ++l) {
@@ -977,6 +1015,8 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   for (uint32_t r = 0; r < GemvPlan::kMaxPf; ++r) a.pf_ptr[r] = p.pf_ptr[r], a.pf_bytes[r] = p.pf_bytes[r];
   a.dbg = dbg;
   a.dbg_global = global_clock;
+  a.peers = PeerOut{};
+  if (peers) a.peers = *peers;
   a.wait_x = (flags & kXIndependent) ? 0u : 1u;
   a.pre = p.pre, a.npre_max = p.npre_max, a.x_first = p.x_first, a.x_gate = p.x_gate;
   a.repeat = repeat;
@@ -985,7 +1025,9 @@ int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint3
   std::copy(p.cta_q1, p.cta_q1 + p.grid, a.cta_q1);
   std::copy(p.cta_e0, p.cta_e0 + p.grid, a.cta_e0);
   std::copy(p.cta_e1, p.cta_e1 + p.grid, a.cta_e1);
-  const GemvFn fn = (p.teams == 2 || p.wide) ? pick_teams(p.kmax) : pick_kernel(p.kmax, p.uniform_rb, p.xsm);
+  if (a.peers.n && !p.uniform_rb) return (int)cudaErrorNotSupported;  // (exchange variants: group2 % 4 == 0)
+  const GemvFn fn = a.peers.n ? pick_peer(p.kmax, p.xsm, p.teams == 2 || p.wide)
+                              : (p.teams == 2 || p.wide) ? pick_teams(p.kmax) : pick_kernel(p.kmax, p.uniform_rb, p.xsm);
   const uint32_t threads = (p.warps * p.teams + 2) * 32;
   void* params[] = {&a};
   return (int)launch_ex((const void*)fn, dim3(p.grid), dim3(threads), p.smem, (cudaStream_t)stream, pdl, params);

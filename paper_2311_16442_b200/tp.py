@@ -60,25 +60,121 @@ def shard_layer(layer: PackedLayer, rank: int, world: int, mode: str):
 
 
 class TPLinear:
-    """One rank's shard of a quantized linear + the collective that completes it."""
+    """One rank's shard of a quantized linear + the exchange that completes it.
+
+    exchange="collective": NCCL all-gather / all-reduce (or gloo through host
+    memory in the CPU harness).  exchange="peer" (batch 1; larger batches use
+    the collective): the exchange is fused with the GEMV -- the kernel's
+    epilogue stores this rank's rows straight into every rank's buffer
+    (column split: its rows of every rank's full y; row split: its partial
+    into its slot of every rank's staging buffer) over CUDA IPC mappings
+    (NVLink P2P between GPUs) and adds its CTAs' arrivals to every rank's
+    counter; one stream-ordered wait (and, for the row split, the rank-order
+    sum of the slots) completes it.  The buffers are exchanged once, at
+    construction, through the process group (collective call: every rank
+    constructs its TPLinear together).  The returned y is this layer's
+    buffer, rewritten by its next call.  One rank per GPU (the wait kernel
+    spins until the other ranks' kernels have pushed; ranks sharing a GPU
+    from separate processes would need MPS to run concurrently -- the tests
+    run such ranks as streams of one process, tests/test_tp.py)."""
 
     def __init__(self, layer: PackedLayer, rank: int, world: int, mode: str, device=None,
-                 kernel: str = "auto"):
+                 kernel: str = "auto", exchange: str = "collective", group=None):
         import torch
 
         from .engine import DeviceLayer
-        self.mode, self.rank, self.world = mode, rank, world
+        if exchange not in ("collective", "peer"):
+            raise ValueError("exchange must be 'collective' or 'peer'")
+        self.mode, self.rank, self.world, self.exchange = mode, rank, world, exchange
         self.rows, self.cols = layer.cfg.rows, layer.cfg.cols
         self.shard, self.ranges, self.idx = shard_layer(layer, rank, world, mode)
         self.torch = torch
         dev = torch.device(device if device is not None else "cuda")
         index = dev.index if dev.index is not None else torch.cuda.current_device()
         self.device = torch.device("cuda", index)
-        self.dl = DeviceLayer(self.shard, index, kernel=kernel)
+        # the fused exchange runs on the SIMT kernel
+        self.dl = DeviceLayer(self.shard, index, kernel="simt" if exchange == "peer" else kernel)
         if self.idx is not None:
             # one gather from x padded with a zero column: pads read it
             self.gidx = torch.from_numpy(np.where(self.idx >= 0, self.idx, self.cols)).to(self.device)
         self.max_rows = max(r1 - r0 for r0, r1 in self.ranges) if mode == "col" else self.rows
+        if exchange == "peer":
+            self._bind_peers(group)
+
+    def _bind_peers(self, group):
+        """Allocate this rank's exchange buffers, swap CUDA IPC handles with
+        the other ranks and point the kernel's peer stores at their buffers."""
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from ._native import check, lib
+        torch = self.torch
+        n = self.rows if self.mode == "col" else self.world * self.rows
+        self.xbuf = torch.zeros(n, dtype=torch.float32, device=self.device)      # full y / staging slots
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)        # arrival counter
+        self.y_out = self.xbuf if self.mode == "col" else torch.zeros(self.rows, dtype=torch.float32,
+                                                                       device=self.device)
+        self.y_loc = torch.zeros(self.dl.rows, dtype=torch.float32, device=self.device)
+        torch.cuda.synchronize(self.device)
+
+        def handle(t):
+            h = C.create_string_buffer(64)
+            check(lib().qw_ipc_handle(C.c_void_p(t.data_ptr()), h))
+            return h.raw
+
+        mine = (handle(self.xbuf), handle(self.flag), int(lib().qw_push_arrivals(self.dl._h)))
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.expected = sum(e[2] for e in everyone)
+        self._opened = []
+        ys, flags = [], []
+        for r, (hb, hf, _) in enumerate(everyone):
+            if r == self.rank:
+                base, fl = self.xbuf.data_ptr(), self.flag.data_ptr()
+            else:
+                pb, pf = C.c_void_p(), C.c_void_p()
+                check(lib().qw_ipc_open(hb, C.byref(pb)))
+                check(lib().qw_ipc_open(hf, C.byref(pf)))
+                self._opened += [pb.value, pf.value]
+                base, fl = pb.value, pf.value
+            off = self.ranges[self.rank][0] if self.mode == "col" else self.rank * self.rows
+            ys.append(base + 4 * off)
+            flags.append(fl)
+        self._peer_y = (C.c_void_p * self.world)(*ys)
+        self._peer_flag = (C.c_void_p * self.world)(*flags)
+        dist.barrier(group=group)
+
+    def close(self):
+        """Unmap the peers' buffers (peer exchange)."""
+        import ctypes as C
+
+        from ._native import lib
+        for p in getattr(self, "_opened", []):
+            lib().qw_ipc_close(C.c_void_p(p))
+        self._opened = []
+
+    def _forward_peer(self, xb):
+        """Batch 1 over peer memory: one fused GEMV + exchange launch, the wait
+        for every rank's arrivals, and (row split) the rank-order sum."""
+        import ctypes as C
+
+        from ._native import check, lib
+        from .engine import _stream_handle
+        torch = self.torch
+        stream = C.c_void_p(_stream_handle(None))
+        if self.mode == "col":
+            x = xb.reshape(-1).contiguous()
+        else:
+            xp = torch.cat([xb, torch.zeros(1, 1, dtype=xb.dtype, device=self.device)], dim=1)
+            x = xp.index_select(1, self.gidx).reshape(-1).contiguous()
+        check(lib().qw_matvec_push(self.dl._h, C.c_void_p(x.data_ptr()), C.c_void_p(self.y_loc.data_ptr()),
+                                   self._peer_y, self._peer_flag, self.world, stream, 0))
+        check(lib().qw_peer_wait(C.c_void_p(self.flag.data_ptr()), self.expected, stream))
+        if self.mode == "row":
+            check(lib().qw_peer_reduce(C.c_void_p(self.xbuf.data_ptr()), self.world, self.rows,
+                                       C.c_void_p(self.y_out.data_ptr()), stream))
+        return self.y_out.reshape(1, -1)
 
     def _collective(self, fn, *tensors, group=None):
         """Run a collective on device tensors (NCCL) or, for a gloo group,
@@ -100,6 +196,9 @@ class TPLinear:
         squeeze = x.dim() == 1
         xb = (x.reshape(1, -1) if squeeze else x).to(self.device)
         b = xb.shape[0]
+        if self.exchange == "peer" and b == 1:
+            y = self._forward_peer(xb)
+            return y.reshape(-1) if squeeze else y
         if self.mode == "col":
             r0, r1 = self.ranges[self.rank]
             y_loc = torch.zeros(b, self.max_rows, dtype=torch.float32, device=self.device)

@@ -144,3 +144,120 @@ def test_tp_forward_on_gpu_ranks(world, rows, cols, batch, group2, mode):
         ref = oracle.matvec_f64(layer, qw.synth_activation(cols, 77 + b))
         err = float(np.linalg.norm(y[b] - ref) / np.linalg.norm(ref))
         assert err <= 1e-2, (b, err)
+
+
+# ------------------------------------------- the exchange fused with the GEMV
+def _peer_ranks_in_one_process(layer, world, mode, x):
+    """The fused GEMV + peer-memory exchange with `world` ranks as streams of
+    ONE process on cuda:0 (same-device ranks in separate processes would need
+    MPS for their kernels to run concurrently; between GPUs the peer pointers
+    are NVLink P2P / IPC mappings and the kernels are the same).  Returns
+    every rank's y."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2311_16442_b200._native import check, lib
+    from paper_2311_16442_b200.tp import shard_layer
+    dls, xs, bufs, flags, ranges = [], [], [], [], None
+    for r in range(world):
+        shard, ranges_r, idx = shard_layer(layer, r, world, mode)
+        ranges = ranges_r or ranges
+        dls.append(qw.DeviceLayer(shard, 0, kernel="simt"))
+        if mode == "col":
+            xs.append(torch.from_numpy(x).cuda())
+        else:
+            xp = np.concatenate([x, [0.0]]).astype(np.float32)
+            xs.append(torch.from_numpy(xp[np.where(idx >= 0, idx, len(x))]).cuda())
+        n = layer.cfg.rows if mode == "col" else world * layer.cfg.rows
+        bufs.append(torch.zeros(n, dtype=torch.float32, device="cuda"))
+        flags.append(torch.zeros(1, dtype=torch.int32, device="cuda"))
+    expected = sum(int(lib().qw_push_arrivals(d._h)) for d in dls)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    ys = [torch.zeros(layer.cfg.rows, dtype=torch.float32, device="cuda") for _ in range(world)]
+    torch.cuda.synchronize()
+    y_loc = [torch.zeros(d.rows, dtype=torch.float32, device="cuda") for d in dls]
+    # every push is enqueued before any wait: streams of one process may share
+    # a hardware queue, and a spinning wait must not sit ahead of a push
+    for r in range(world):
+        off = ranges[r][0] if mode == "col" else r * layer.cfg.rows
+        peer_y = (C.c_void_p * world)(*[b.data_ptr() + 4 * off for b in bufs])
+        peer_f = (C.c_void_p * world)(*[f.data_ptr() for f in flags])
+        check(lib().qw_matvec_push(dls[r]._h, C.c_void_p(xs[r].data_ptr()), C.c_void_p(y_loc[r].data_ptr()),
+                                   peer_y, peer_f, world, C.c_void_p(streams[r].cuda_stream), 0))
+    for r in range(world):
+        st = C.c_void_p(streams[r].cuda_stream)
+        check(lib().qw_peer_wait(C.c_void_p(flags[r].data_ptr()), expected, st))
+        if mode == "row":
+            check(lib().qw_peer_reduce(C.c_void_p(bufs[r].data_ptr()), world, layer.cfg.rows,
+                                       C.c_void_p(ys[r].data_ptr()), st))
+    torch.cuda.synchronize()
+    assert all(int(f.item()) == 0 for f in flags)  # every wait took its arrivals off
+    return [(b if mode == "col" else y).cpu().numpy() for b, y in zip(bufs, ys)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["col", "row"])
+@pytest.mark.parametrize("world,rows,cols", [(2, 512, 1024), (3, 11008 // 8, 4096), (4, 384, 2048)])
+def test_tp_peer_exchange_fused_with_the_gemv(world, rows, cols, mode):
+    """qw_matvec_push (the GEMV whose epilogue stores into every rank's
+    buffer and counts its CTAs' arrivals there) + qw_peer_wait (+ the
+    rank-order qw_peer_reduce for the row split): every rank ends with the
+    full y, equal across ranks and within 1e-2 of the unsharded oracle, for
+    two calls in a row (the counters need no reset)."""
+    layer = qw.synth_layer(rows, cols, seed=rows + cols + 5, outlier_ratio=0.01)
+    for k in range(2):
+        x = qw.synth_activation(cols, 80 + k)
+        ys = _peer_ranks_in_one_process(layer, world, mode, x)
+        ref = oracle.matvec_f64(layer, x)
+        for r in range(world):
+            err = float(np.linalg.norm(ys[r] - ref) / np.linalg.norm(ref))
+            assert err <= 1e-2, (r, k, err)
+            assert np.array_equal(ys[r], ys[0])
+
+
+def _ipc_worker(rank, port, q):
+    """Rank 1 maps rank 0's buffer through its CUDA IPC handle and writes into
+    it (qw_peer_reduce with one slot); rank 0 reads the values back."""
+    import ctypes as C
+
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2311_16442_b200._native import check, lib
+        buf = torch.zeros(1000, dtype=torch.float32, device="cuda:0")
+        torch.cuda.synchronize()
+        h = C.create_string_buffer(64)
+        check(lib().qw_ipc_handle(C.c_void_p(buf.data_ptr()), h))
+        handles = [None, None]
+        dist.all_gather_object(handles, h.raw)
+        if rank == 1:
+            src = torch.arange(1000, dtype=torch.float32, device="cuda:0") * 0.5
+            p = C.c_void_p()
+            check(lib().qw_ipc_open(handles[0], C.byref(p)))
+            check(lib().qw_peer_reduce(C.c_void_p(src.data_ptr()), 1, 1000, p, None))
+            torch.cuda.synchronize()
+            check(lib().qw_ipc_close(p))
+        dist.barrier()
+        if rank == 0:
+            q.put(buf.cpu().numpy())
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_ipc_handles_map_a_peer_buffer():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert np.array_equal(got, np.arange(1000, dtype=np.float32) * 0.5)
