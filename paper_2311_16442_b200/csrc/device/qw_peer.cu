@@ -17,6 +17,10 @@ namespace {
 // take them off the counter -- arrivals of the next launch that raced ahead
 // stay counted, so the counter needs no reset and CUDA-graph replays work
 __global__ void peer_wait_kernel(uint32_t* flag, uint32_t expected) {
+  // the next kernel may launch (and stream its weights) now: it reads y only
+  // after this grid completes (griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x != 0) return;
   uint32_t seen = 0;
   do {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(flag) : "memory");
@@ -36,8 +40,18 @@ __global__ void peer_reduce_kernel(const float* __restrict__ staging, uint32_t w
 }  // namespace
 
 int launch_peer_wait(uint32_t* flag, uint32_t expected, void* stream) {
-  peer_wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag, expected);
-  return (int)cudaGetLastError();
+  // programmatic dependent launch: the wait only polls the counter, so it
+  // starts under the push kernel instead of after it
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, peer_wait_kernel, flag, expected);
 }
 
 int launch_peer_reduce(const float* staging, uint32_t world, uint32_t n, float* y, void* stream) {
