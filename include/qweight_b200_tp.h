@@ -40,6 +40,18 @@ int qw_tp_create(const qw_host_layer* layer, int rank, int world, int mode, int 
  * order, identical on every rank), y device fp32 [batch][rows] (the full
  * output on every rank).  batch 1..16. */
 int qw_tp_matvec(qw_tp* tp, const float* x, uint32_t batch, float* y, ncclComm_t comm, void* stream);
+/* The same exchange without NCCL, fused with the GEMV over peer memory
+ * (batch 1; the shard must run the SIMT kernel: create with QW_UPLOAD_SIMT).
+ * Each rank allocates an exchange buffer of qw_tp_exchange_bytes and a
+ * zeroed uint32 arrival counter, maps the other ranks' buffers and counters
+ * (qw_ipc_handle / qw_ipc_open, NVLink P2P), and binds them in rank order;
+ * `expected` is the sum over the ranks of qw_tp_arrivals.  qw_tp_matvec_peer
+ * then runs qw_matvec_push into every rank's buffer, the wait on this rank's
+ * counter, and (row split) the rank-order sum; y: device fp32 [rows]. */
+int qw_tp_exchange_bytes(const qw_tp* tp, uint64_t* bytes);
+int qw_tp_arrivals(const qw_tp* tp);
+int qw_tp_bind_peers(qw_tp* tp, float* const* peer_buf, uint32_t* const* peer_flag, uint32_t expected);
+int qw_tp_matvec_peer(qw_tp* tp, const float* x, float* y, void* stream);
 /* Rows this rank computes (column split) or the shard's input channels (row split). */
 int qw_tp_local_extent(const qw_tp* tp, uint32_t* rows, uint32_t* cols);
 int qw_tp_free(qw_tp* tp);

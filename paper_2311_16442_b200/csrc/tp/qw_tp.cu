@@ -29,6 +29,12 @@ struct qw_tp {
   float* d_xs = nullptr;           // row split: the shard's input [16][scols]
   float* d_yloc = nullptr;         // column split: [16][max_rows] padded local y
   float* d_gather = nullptr;       // column split: [world][16][max_rows]
+  // peer-memory exchange (qw_tp_bind_peers)
+  std::vector<float*> peer_y;      // where this rank's rows / partial go in each rank's buffer
+  std::vector<uint32_t*> peer_flag;
+  float* own_buf = nullptr;
+  uint32_t* own_flag = nullptr;
+  uint32_t expected = 0;
   ~qw_tp() {
     if (shard) qw_layer_free(shard);
     if (ws) qw_workspace_free(ws);
@@ -151,6 +157,54 @@ int qw_tp_matvec(qw_tp* T, const float* x, uint32_t batch, float* y, ncclComm_t 
     if (int s = qw_matvec(T->shard, T->d_xs, batch, y, T->ws, stream)) return s;
     if (int s = nccl_status(ncclAllReduce(y, y, (size_t)batch * T->rows, ncclFloat32, ncclSum, comm, st)))
       return s;
+  }
+  return cudaGetLastError() == cudaSuccess ? QW_OK : QW_ERR_CUDA;
+}
+
+int qw_tp_exchange_bytes(const qw_tp* T, uint64_t* bytes) {
+  if (!T || !bytes) return QW_ERR_ARG;
+  *bytes = (uint64_t)4 * T->rows * (T->mode == QW_TP_COLUMN ? 1u : (uint32_t)T->world);
+  return QW_OK;
+}
+
+int qw_tp_arrivals(const qw_tp* T) { return T ? qw_push_arrivals(T->shard) : -QW_ERR_ARG; }
+
+int qw_tp_bind_peers(qw_tp* T, float* const* peer_buf, uint32_t* const* peer_flag, uint32_t expected) {
+  if (!T || !peer_buf || !peer_flag || expected == 0) return QW_ERR_ARG;
+  if (qw_layer_uses_tensor_core(T->shard)) return QW_ERR_UNSUPPORTED;  // the exchange runs on the SIMT kernel
+  T->peer_y.clear(), T->peer_flag.clear();
+  for (int r = 0; r < T->world; ++r) {
+    if (!peer_buf[r] || !peer_flag[r]) return QW_ERR_ARG;
+    const uint32_t off = T->mode == QW_TP_COLUMN ? T->ranges[2 * T->rank] : (uint32_t)T->rank * T->rows;
+    T->peer_y.push_back(peer_buf[r] + off);
+    T->peer_flag.push_back(peer_flag[r]);
+  }
+  T->own_buf = peer_buf[T->rank], T->own_flag = peer_flag[T->rank], T->expected = expected;
+  return QW_OK;
+}
+
+int qw_tp_matvec_peer(qw_tp* T, const float* x, float* y, void* stream) {
+  if (!T || !x || !y) return QW_ERR_ARG;
+  if (T->peer_y.empty()) return QW_ERR_ARG;  // not bound
+  cudaSetDevice(T->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const float* xin = x;
+  if (T->mode == QW_TP_ROW) {
+    gather_cols<<<std::min<uint32_t>((T->scols + 255) / 256, 1184), 256, 0, st>>>(x, T->cols, T->d_idx, T->scols,
+                                                                                  1, T->d_xs);
+    xin = T->d_xs;
+  }
+  // the shard's own result goes to scratch (the exchange buffers hold the output)
+  float* ytmp = T->mode == QW_TP_COLUMN ? T->d_gather : y;
+  if (int s = qw_matvec_push(T->shard, xin, ytmp, T->peer_y.data(), T->peer_flag.data(), (uint32_t)T->world, stream,
+                             QW_LAUNCH_PDL))
+    return s;
+  if (int s = qw_peer_wait(T->own_flag, T->expected, stream)) return s;
+  if (T->mode == QW_TP_COLUMN) {
+    if (cudaMemcpyAsync(y, T->own_buf, (size_t)4 * T->rows, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return QW_ERR_CUDA;
+  } else if (int s = qw_peer_reduce(T->own_buf, (uint32_t)T->world, T->rows, y, stream)) {
+    return s;
   }
   return cudaGetLastError() == cudaSuccess ? QW_OK : QW_ERR_CUDA;
 }

@@ -116,11 +116,12 @@ def test_diagnostic_knobs_are_inert_without_the_debug_gate():
 
 
 def test_tp_library_exports_its_header():
-    """include/qweight_b200_tp.h <-> libqweight_b200_tp.so (NCCL entries)."""
+    """include/qweight_b200_tp.h <-> libqweight_b200_tp.so (NCCL and peer-exchange entries)."""
     tp_h = ROOT / "include" / "qweight_b200_tp.h"
     text = re.sub(r"/\*.*?\*/", "", tp_h.read_text(), flags=re.S)
     declared = set(re.findall(r"\b(qw_tp_[a-z0-9_]+)\s*\(", text))
-    assert declared == {"qw_tp_create", "qw_tp_matvec", "qw_tp_local_extent", "qw_tp_free"}
+    assert declared == {"qw_tp_create", "qw_tp_matvec", "qw_tp_local_extent", "qw_tp_free",
+                        "qw_tp_exchange_bytes", "qw_tp_arrivals", "qw_tp_bind_peers", "qw_tp_matvec_peer"}
     lib = _native.lib_path().parent / "libqweight_b200_tp.so"
     out = subprocess.run(["nm", "-D", "--defined-only", str(lib)], capture_output=True, text=True, check=True).stdout
     exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}

@@ -54,3 +54,39 @@ def test_tp_c_abi_single_rank_nccl(mode, batch):
     assert rows.value == 384
     tp_lib.qw_tp_free(tp)
     nccl.ncclCommDestroy(comm)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_tp_c_abi_peer_exchange_single_rank(mode):
+    """qw_tp_bind_peers / qw_tp_matvec_peer: the exchange fused with the GEMV
+    over peer memory, one rank (it pushes into its own buffer and waits for
+    its own arrivals; the multi-rank protocol is tests/test_tp.py), twice."""
+    import torch
+    qw.lib()
+    tp_lib = C.CDLL(str(TP_LIB))
+    layer = qw.synth_layer(384, 1024, seed=93, outlier_ratio=0.005)
+    h = layer._handle()
+    tp = C.c_void_p()
+    try:
+        assert tp_lib.qw_tp_create(h, 0, 1, mode, 0, 2, C.byref(tp)) == 0  # QW_UPLOAD_SIMT
+    finally:
+        qw.lib().qw_host_free(h)
+    nbytes = C.c_uint64()
+    assert tp_lib.qw_tp_exchange_bytes(tp, C.byref(nbytes)) == 0
+    buf = torch.zeros(nbytes.value // 4, dtype=torch.float32, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    arrivals = tp_lib.qw_tp_arrivals(tp)
+    assert arrivals > 0
+    bufs = (C.c_void_p * 1)(buf.data_ptr())
+    flags = (C.c_void_p * 1)(flag.data_ptr())
+    assert tp_lib.qw_tp_bind_peers(tp, bufs, flags, arrivals) == 0
+    for k in range(2):
+        x = torch.from_numpy(qw.synth_activation(1024, 94 + k)).cuda()
+        y = torch.empty(384, device="cuda")
+        assert tp_lib.qw_tp_matvec_peer(tp, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                        C.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+        torch.cuda.synchronize()
+        ref = oracle.matvec_f64(layer, qw.synth_activation(1024, 94 + k))
+        assert np.linalg.norm(y.cpu().numpy() - ref) / np.linalg.norm(ref) <= 1e-2
+        assert int(flag.item()) == 0
+    tp_lib.qw_tp_free(tp)
