@@ -23,7 +23,10 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__cycles_elapsed.avg", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "smsp__inst_executed_pipe_fma.sum", "smsp__inst_executed_pipe_alu.sum",
-        "smsp__inst_executed_pipe_lsu.sum", "lts__t_bytes.sum"]
+        "smsp__inst_executed_pipe_lsu.sum", "lts__t_bytes.sum",
+        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active"]
 for r in rows:
     print(r[h.index("Kernel Name")][:60])
     for k in keys:
