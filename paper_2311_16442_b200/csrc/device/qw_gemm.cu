@@ -554,17 +554,30 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       __threadfence();
       const uint32_t st = sg ? tile1 : tile;
       const float* part = a.partial + (size_t)st * a.kmax * kTileRows * 16;
-      for (uint32_t i = threadIdx.x; i < kTileRows * a.batch; i += blockDim.x) {
-        const uint32_t t = i % kTileRows, n = i / kTileRows, row = st * kTileRows + t;
-        float v[kStreamMaxK];  // all slots in flight, then summed in contributor order
+      // item = (row, 4 columns): one float4 per contributor slot, all in
+      // flight, summed in contributor order (one pass: <= 128 x 4 items)
+      const uint32_t nc4 = (a.batch + 3) / 4;
+      for (uint32_t i = threadIdx.x; i < kTileRows * nc4; i += blockDim.x) {
+        const uint32_t t = i % kTileRows, c4 = i / kTileRows, row = st * kTileRows + t;
+        float4 v[kStreamMaxK];
 #pragma unroll
         for (uint32_t k = 0; k < kStreamMaxK; ++k)
-          v[k] = k < nc ? __ldcg(part + ((size_t)k * kTileRows + t) * 16 + n) : 0.0f;
-        float sum = v[0];
+          v[k] = k < nc ? __ldcg(reinterpret_cast<const float4*>(part + ((size_t)k * kTileRows + t) * 16) + c4)
+                        : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        float csr[4];
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+          csr[q] = (row < G.rows && 4 * c4 + q < a.batch) ? __ldg(a.ycsr + (size_t)(4 * c4 + q) * G.rows + row) : 0.0f;
+        float4 sum = v[0];
 #pragma unroll
         for (uint32_t k = 1; k < kStreamMaxK; ++k)
-          if (k < nc) sum += v[k];
-        if (row < G.rows) a.y[(size_t)n * G.rows + row] = sum + __ldg(a.ycsr + (size_t)n * G.rows + row);
+          if (k < nc) sum.x += v[k].x, sum.y += v[k].y, sum.z += v[k].z, sum.w += v[k].w;
+        if (row < G.rows) {
+          const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+          for (uint32_t q = 0; q < 4; ++q)
+            if (4 * c4 + q < a.batch) a.y[(size_t)(4 * c4 + q) * G.rows + row] = sv[q] + csr[q];
+        }
       }
       if (threadIdx.x == 0) a.counters[st] = 0;  // every contributor has arrived: reset for the next call
     }
