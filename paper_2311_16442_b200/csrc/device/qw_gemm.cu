@@ -586,10 +586,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     // the dense sum, then the outliers (row_fma, engine.cpp:111-122): their
     // per-row CSR sums (exact fp32, CSR order) come from the prologue kernel
     pdl_wait();
-    for (uint32_t i = threadIdx.x; i < kTileRows * a.batch; i += blockDim.x) {
-      const uint32_t t = i % kTileRows, n = i / kTileRows, row = tile * kTileRows + t;
-      if (row < G.rows)
-        a.y[(size_t)n * G.rows + row] = s_dense[t * kDenseStride + n] + __ldg(a.ycsr + (size_t)n * G.rows + row);
+    // item = (row, 4 columns): the CSR sums loaded together, one pass
+    const uint32_t nc4 = (a.batch + 3) / 4;
+    for (uint32_t i = threadIdx.x; i < kTileRows * nc4; i += blockDim.x) {
+      const uint32_t t = i % kTileRows, c4 = i / kTileRows, row = tile * kTileRows + t;
+      if (row >= G.rows) continue;
+      float csr[4];
+#pragma unroll
+      for (uint32_t q = 0; q < 4; ++q)
+        csr[q] = 4 * c4 + q < a.batch ? __ldg(a.ycsr + (size_t)(4 * c4 + q) * G.rows + row) : 0.0f;
+#pragma unroll
+      for (uint32_t q = 0; q < 4; ++q)
+        if (4 * c4 + q < a.batch)
+          a.y[(size_t)(4 * c4 + q) * G.rows + row] = s_dense[t * kDenseStride + 4 * c4 + q] + csr[q];
     }
   } else {
     // split-K: the tile's K splits form one thread-block cluster; CTA `split`
