@@ -344,10 +344,11 @@ int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
 bool uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
   static const uint32_t forced = qwdev::knob("QW_GEMM_MIN_BATCH", 0);
   if (batch < 2 || !L->dev.gemm.ok || (flags & QW_LAUNCH_FORCE_COLUMNS)) return false;
-  // layers of <= 4096 input channels keep the column launch one column longer
-  // (q/k/v/o and gate/up at b = 6: 13.1 vs 14.6 / 29.1 vs 29.2 us; the
-  // 11008-channel down_proj crosses at 6: 30.1 vs 26.8 us)
-  const uint32_t min_batch = forced ? forced : QW_GEMM_MIN_BATCH + (L->dev.g.cols <= 4096 ? 1u : 0u);
+  // layers of at most 4096 x 4096 weights keep the column launch one column
+  // longer (q/k/v/o at b = 6: 13.1 vs 14.5 us; gate/up and down_proj cross at
+  // 6: 29.1 vs 28.5 and 30.1 vs 26.1 us)
+  const uint64_t weights = (uint64_t)L->dev.g.rows * L->dev.g.cols;
+  const uint32_t min_batch = forced ? forced : QW_GEMM_MIN_BATCH + (weights <= 4096ull * 4096ull ? 1u : 0u);
   return (flags & QW_LAUNCH_FORCE_GEMM) || batch >= min_batch;
 }
 
