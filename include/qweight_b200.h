@@ -217,7 +217,7 @@ int qw_matvec_pdl(const qw_layer* layer, const float* x, uint32_t batch,
  * read from HBM about once and shared through L2).  The crossover is
  * measured (profiles/r02_batch_sweep_*.jsonl).  These flags force one or the
  * other. */
-#define QW_GEMM_MIN_BATCH 6u /* + 1 for layers of at most 4096 x 4096 weights */
+#define QW_GEMM_MIN_BATCH 6u
 #define QW_LAUNCH_FORCE_GEMM 4u
 #define QW_LAUNCH_FORCE_COLUMNS 8u
 int qw_matvec_ex(const qw_layer* layer, const float* x, uint32_t batch, float* y,

@@ -339,16 +339,13 @@ int check_ws(const qw_layer* L, const qw_workspace* ws, uint32_t batch) {
 
 // batched policy (qweight_b200.h): K4 from QW_GEMM_MIN_BATCH columns up, the
 // batch-1 kernel over the columns (8 to a launch) below -- up to 5 columns
-// one column launch beats K4 on every 7B shape; at 6 columns K4 wins on
-// down_proj, ties on gate/up and loses on q_proj (profiles/r02_batch_sweep_simt.jsonl)
+// one column launch beats K4 on every 7B shape; from 6 columns K4 wins
+// (q_proj 12.7 vs 13.2 us, gate/up 28.3 vs 29.1, down_proj 25.7 vs 30.6;
+// profiles/r02_batch_sweep_simt.jsonl)
 bool uses_gemm(const qw_layer* L, uint32_t batch, uint32_t flags) {
   static const uint32_t forced = qwdev::knob("QW_GEMM_MIN_BATCH", 0);
   if (batch < 2 || !L->dev.gemm.ok || (flags & QW_LAUNCH_FORCE_COLUMNS)) return false;
-  // layers of at most 4096 x 4096 weights keep the column launch one column
-  // longer (q/k/v/o at b = 6: 13.1 vs 14.5 us; gate/up and down_proj cross at
-  // 6: 29.1 vs 28.5 and 30.1 vs 26.1 us)
-  const uint64_t weights = (uint64_t)L->dev.g.rows * L->dev.g.cols;
-  const uint32_t min_batch = forced ? forced : QW_GEMM_MIN_BATCH + (weights <= 4096ull * 4096ull ? 1u : 0u);
+  const uint32_t min_batch = forced ? forced : QW_GEMM_MIN_BATCH;
   return (flags & QW_LAUNCH_FORCE_GEMM) || batch >= min_batch;
 }
 

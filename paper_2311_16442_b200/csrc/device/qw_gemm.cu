@@ -115,44 +115,55 @@ __device__ __forceinline__ float p2(int e) { return __uint_as_float((uint32_t)(m
 // converts kPrepPer elements per thread (independent loads, so no thread waits
 // on a chain); few enough CTAs to run in one wave beside the GEMM's.
 constexpr uint32_t kPrepThreads = 256, kPrepPer = 4;
+constexpr uint32_t kPrepPdlMaxBlocks = 192;  // launch_gemm: PDL for the x prologue up to this grid
 // CSR outliers of every row for all columns: y_csr[n][r] = sum over the row's
 // entries, in CSR order, of fp16(v) * x_n[perm[col]] (sparse_matvec,
 // outliers.cpp:131-141), exact fp32.  One thread per (row, column); the row's
 // entries are loaded first so the x gathers are independent.
-__device__ __forceinline__ void csr_row(const float* __restrict__ xn, const uint16_t* __restrict__ perm,
-                                        const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ csr,
-                                        uint32_t rows, float* __restrict__ yn, uint32_t row) {
-  if (row >= rows) return;
-  const uint32_t e0 = __ldg(row_ptr + row), e1 = __ldg(row_ptr + row + 1);
+constexpr uint32_t kCsrRound = 24;
+__device__ __forceinline__ void csr_row(const float* __restrict__ xn, const uint32_t* __restrict__ row_ptr,
+                                        const uint32_t* __restrict__ csr, uint32_t rows, float* __restrict__ yn,
+                                        uint32_t row) {
+  // the row's bounds and first kCsrRound entries are layer constants: loaded before
+  // the dependency wait (under the previous kernel), only the x gathers after
+  uint32_t e0 = 0, e1 = 0;
+  if (row < rows) e0 = __ldg(row_ptr + row), e1 = __ldg(row_ptr + row + 1);
   float acc = 0.0f;
-  // 32 entries per round: a row of <= 32 outliers costs two dependent loads
-  for (uint32_t e = e0; e < e1; e += 32) {
-    uint32_t ent[32];
+  // kCsrRound entries per round: a row of <= kCsrRound outliers costs one load
+  // after the wait
+  for (uint32_t e = e0, first = 1; first || e < e1; e += kCsrRound, first = 0) {
+    uint32_t ent[kCsrRound];
 #pragma unroll
-    for (int u = 0; u < 32; ++u) ent[u] = e + u < e1 ? __ldg(csr + e + u) : 0u;
-    float p[32];
+    for (int u = 0; u < (int)kCsrRound; ++u) ent[u] = e + u < e1 ? __ldg(csr + e + u) : 0u;
+    if (first) pdl_wait();  // x is the previous kernel's output
+    if (e >= e1) break;
+    float p[kCsrRound];
 #pragma unroll
-    for (int u = 0; u < 32; ++u)
+    for (int u = 0; u < (int)kCsrRound; ++u)
       p[u] = __fmul_rn(half_bits_to_float(ent[u] >> 16), __ldg(xn + (ent[u] & 0xFFFFu)));  // original channel
 #pragma unroll
-    for (int u = 0; u < 32; ++u)
+    for (int u = 0; u < (int)kCsrRound; ++u)
       if (e + u < e1) acc = __fadd_rn(acc, p[u]);
   }
-  yn[row] = acc;
+  if (row < rows) yn[row] = acc;
 }
 
-__global__ void __launch_bounds__(kPrepThreads) xprep_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(kPrepThreads, 4) xprep_kernel(const float* __restrict__ x,
                                                              const uint16_t* __restrict__ perm, Geometry G,
                                                              uint32_t stages, uint32_t batch,
                                                              uint16_t* __restrict__ xpt, int* __restrict__ xexp,
                                                              uint32_t chunks, const uint32_t* __restrict__ row_ptr,
                                                              const uint32_t* __restrict__ csr,
                                                              float* __restrict__ ycsr) {
+  // launched with PDL: resident under the previous kernel; layer constants
+  // (perm, CSR) are read before griddepcontrol.wait, x after it
   pdl_launch_dependents();  // the GEMM's weight stream does not depend on us
   if (blockIdx.x >= chunks) {  // CSR blocks: one row of column blockIdx.y per thread
     if (blockIdx.y < batch)
-      csr_row(x + (size_t)blockIdx.y * G.cols, perm, row_ptr, csr, G.rows, ycsr + (size_t)blockIdx.y * G.rows,
+      csr_row(x + (size_t)blockIdx.y * G.cols, row_ptr, csr, G.rows, ycsr + (size_t)blockIdx.y * G.rows,
               (blockIdx.x - chunks) * kPrepThreads + threadIdx.x);
+    else
+      pdl_wait();
     return;
   }
   const uint32_t n = blockIdx.y;
@@ -161,17 +172,21 @@ __global__ void __launch_bounds__(kPrepThreads) xprep_kernel(const float* __rest
   const uint32_t n2 = G.cols - G.n4;
   // the gathered elements are loaded before / beside the max pass (only the
   // scale depends on the max): two dependent loads per thread in total
-  float xv[kPrepPer];
+  uint32_t ch[kPrepPer];
 #pragma unroll
   for (uint32_t u = 0; u < kPrepPer; ++u) {
     const uint32_t i = (blockIdx.x * kPrepPer + u) * kPrepThreads + threadIdx.x;
-    xv[u] = 0.0f;
+    ch[u] = 0xFFFFFFFFu;
     if (i < stages * kStageK && n < batch) {
       const uint32_t st = i / kStageK, k = i % kStageK;
       const uint32_t slot = k < 96 ? 96 * st + k : G.n2p + 32 * st + (k - 96);
-      if (!(slot >= n2 && slot < G.n2p)) xv[u] = __ldg(xn + __ldg(perm + slot));
+      if (!(slot >= n2 && slot < G.n2p)) ch[u] = __ldg(perm + slot);
     }
   }
+  pdl_wait();  // x is the previous kernel's output
+  float xv[kPrepPer];
+#pragma unroll
+  for (uint32_t u = 0; u < kPrepPer; ++u) xv[u] = ch[u] != 0xFFFFFFFFu ? __ldg(xn + ch[u]) : 0.0f;
   float m = 0.0f;
   if (n < batch) {
     const uint32_t n4v = G.cols >> 2;  // cols % 16 == 0 (validate_layer)
@@ -531,6 +546,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
   __syncthreads();
   if (threadIdx.x == 0) gstamp(a, 2);  // CTA joined after the accumulator read
+  // the next launch (its x prologue, PDL) may become resident for our tail:
+  // it reads nothing of ours before its griddepcontrol.wait
+  pdl_launch_dependents();
 
   if (kStream) {
     // stream-K fixup: the last contributor of a tile (arrival counter) sums
@@ -788,10 +806,30 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   // one grid row per live column: the B columns >= batch are never stored
   // (MMA columns are independent), and a small prologue grid leaves the SMs
   // free for the GEMM's CTAs, which launch as soon as it starts (PDL)
-  xprep_kernel<<<dim3(chunks + csr_blocks, batch), kPrepThreads, 0, st>>>(x, L.perm16, G, p.stages, batch, p.xpt,
-                                                                       p.xexp, chunks, L.row_ptr, L.csr, p.ycsr);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return (int)e;
+  static const bool no_pdl = qwdev::knob_str("QW_GEMM_NOPDL") != nullptr;  // diagnostics
+  {
+    // PDL: the prologue's CTAs become resident under the previous kernel and
+    // wait for it in griddepcontrol.wait instead of a launch after it
+    cudaLaunchConfig_t pc = {};
+    pc.gridDim = dim3(chunks + csr_blocks, batch);
+    pc.blockDim = dim3(kPrepThreads);
+    pc.stream = st;
+    cudaLaunchAttribute pa[1];
+    pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pa[0].val.programmaticStreamSerializationAllowed = 1;
+    pc.attrs = pa;
+    // PDL only for a grid that fits beside the running kernel about once per
+    // SM: the prologue CTAs sit resident (blocked in griddepcontrol.wait)
+    // until the previous kernel completes, and an SM holding two of them has
+    // no registers left for a GEMM CTA of the next launch (80 x 576 + 2 x 64
+    // x 256 > 64 K), which then starts late (measured: 4096 x 11008 at b = 8
+    // +8 us with PDL, 4096^2 at b = 2 -2.5 us)
+    const uint32_t nblk = (chunks + csr_blocks) * batch;
+    pc.numAttrs = (no_pdl || nblk > kPrepPdlMaxBlocks) ? 0 : 1;
+    cudaError_t e = cudaLaunchKernelEx(&pc, xprep_kernel, x, (const uint16_t*)L.perm16, G, p.stages, batch, p.xpt,
+                                       p.xexp, chunks, (const uint32_t*)L.row_ptr, (const uint32_t*)L.csr, p.ycsr);
+    if (e != cudaSuccess) return (int)e;
+  }
   GemmArgs a;
   std::memcpy(a.tm, p.tmap, sizeof(a.tm));
   std::memcpy(&a.tso, p.tmap_so, sizeof(a.tso));
@@ -820,7 +858,6 @@ int launch_gemm(const DeviceLayer& L, const float* x, uint32_t batch, float* y, 
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  static const bool no_pdl = qwdev::knob_str("QW_GEMM_NOPDL") != nullptr;  // diagnostics
   cfg.numAttrs = no_pdl ? 1 : 2;
   void* params[] = {&a};
   return (int)cudaLaunchKernelExC(&cfg, use_stream ? (const void*)gemm_kernel<true> : (const void*)gemm_kernel<false>,

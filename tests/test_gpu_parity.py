@@ -207,9 +207,9 @@ def test_batched_tensor_core_path(rows, cols, batch):
     layer = qw.synth_layer(rows, cols, seed=rows + cols + batch, outlier_ratio=0.005)
     dl = qw.DeviceLayer(layer)
     assert dl.launches_per_matvec(batch, "gemm") == 2, "expected x prologue + tcgen05 GEMM"
-    # the default policy: K4 from 6 columns (7 for at most 4096 x 4096
-    # weights), the batch-1 kernel 8 columns to a launch below
-    min_b = 7 if rows * cols <= 4096 * 4096 else 6
+    # the default policy: K4 from 6 columns, the batch-1 kernel 8 columns to
+    # a launch below
+    min_b = 6
     assert dl.batched_path(batch) == ("gemm" if batch >= min_b else "columns")
     assert dl.launches_per_matvec(batch) == (2 if batch >= min_b else (batch + 7) // 8)
     xs = np.stack([qw.synth_activation(cols, 300 + b) for b in range(batch)])
