@@ -229,6 +229,48 @@ def test_batched_tensor_core_path(rows, cols, batch):
         assert rel_l2(Yc[b], oracle.matvec_f64(layer, xs[b])) <= TOL
 
 
+@pytest.mark.parametrize("n,batch", [(2048, 2), (2048, 8), (4096, 16)])
+def test_k4_dependent_chain_with_pdl(n, batch):
+    """K4 calls whose x is the previous call's y, on ONE layer (the x
+    prologue's scratch is reused by every call), launched back to back with
+    programmatic dependent launch -- the prologue grid resident under the
+    previous GEMM and reading the layer constants before its dependency wait
+    (a plain launch above kPrepPdlMaxBlocks = 192 CTAs: the 4096 x 16 case):
+    bit-identical to the same calls synchronised one by one, eager and as a
+    replayed CUDA graph."""
+    torch = _torch()
+    layer = qw.synth_layer(n, n, seed=n + batch, outlier_ratio=0.005)
+    dl = qw.DeviceLayer(layer)
+    X = torch.from_numpy(np.stack([qw.synth_activation(n, 900 + b) for b in range(batch)])).cuda()
+    steps = 6
+    ref = [X]
+    for _ in range(steps):
+        ref.append(dl.matvec(ref[-1], batched="gemm", pdl=True))
+        torch.cuda.synchronize()
+    assert all(bool(torch.isfinite(r).all()) for r in ref)
+    ys = [torch.empty(batch, n, device="cuda") for _ in range(steps)]
+
+    def run():
+        prev = X
+        for i in range(steps):
+            dl.matvec(prev, out=ys[i], batched="gemm", pdl=True)
+            prev = ys[i]
+    run()
+    torch.cuda.synchronize()
+    for i in range(steps):
+        assert torch.equal(ys[i], ref[i + 1]), i
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run()
+    for _ in range(3):
+        for y in ys:
+            y.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for i in range(steps):
+            assert torch.equal(ys[i], ref[i + 1]), i
+
+
 COLUMN_GEOMS = [
     (96, 512, 0.01),      # one chunk, a few CTAs per column
     (1000, 4096, 0.005),  # rows not a multiple of 16 / 4
