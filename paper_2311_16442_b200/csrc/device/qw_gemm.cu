@@ -770,6 +770,11 @@ int plan_gemm(DeviceLayer& L, int num_sms, float max_scale2, float max_s4) {
   if ((e = cudaMalloc((void**)&p.xpt, (size_t)p.stages * kBStageBytes)) != cudaSuccess) return (int)e;
   if ((e = cudaMalloc((void**)&p.xexp, 16 * sizeof(int))) != cudaSuccess) return (int)e;
   if ((e = cudaMalloc((void**)&p.ycsr, (size_t)16 * G.rows * 4)) != cudaSuccess) return (int)e;
+  // zeroed once: a call writes only its `batch` columns of the B tiles and
+  // exponents, the MMA and the epilogue read all 16 (the rest never reach y;
+  // compute-sanitizer initcheck)
+  if ((e = cudaMemset(p.xpt, 0, (size_t)p.stages * kBStageBytes)) != cudaSuccess) return (int)e;
+  if ((e = cudaMemset(p.xexp, 0, 16 * sizeof(int))) != cudaSuccess) return (int)e;
   // the opt-in limits are per device: one bit per device, set under a lock
   static std::mutex attr_mu;
   static uint64_t attr_dev = 0;

@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
         float A[4], Cz[4];
 #pragma unroll
         for (int i = 0; i < (UNI ? 1 : 4); ++i) {
-          const uint32_t rb = row_block(min(r0 + i, seg_rows - 1)) - rb_first;
+          const uint32_t rb = row_block(min(r0 + i, r_end - 1)) - rb_first;  // the staged row blocks only
           const uint32_t e = s_so[rb * G.G2s + gk[k]];
           A[i] = half_bits_to_float(e) * s_scale;  // exact: scale2 * 2^-P
           Cz[i] = -(pow2f(10 - pe[k]) + small_int_to_float(e >> 16));

@@ -92,9 +92,11 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
-// Named barrier over `threads` threads.
+// Named barrier over `threads` threads.  The non-.aligned form: a warp may
+// reach it diverged (lane-dependent loops before it), which bar.sync
+// (= barrier.sync.aligned) does not allow (compute-sanitizer synccheck).
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 __device__ __forceinline__ half2 as_h2(uint32_t u) { return *reinterpret_cast<half2*>(&u); }
