@@ -45,6 +45,7 @@ struct qw_layer {
   float max_scale2 = 0.0f, max_s4 = 0.0f;  // for the batched path's fp16 range
   std::vector<uint32_t> host_row_ptr;       // CSR row pointers (group launch plans)
   qw_layer_info info{};
+  bool k2_ok = true;  // the SIMT batch-1 kernel's shared-memory plan fits (else the layer runs on K2m)
 };
 
 struct qw_group {
@@ -408,10 +409,11 @@ int upload_packed(const qwb::PackedLayer& L, int device, uint32_t flags, qw_laye
     H->host_row_ptr = L.csr.row_ptr;
     if (H->host_row_ptr.empty()) H->host_row_ptr.assign((size_t)L.cfg.rows + 1, 0u);
     if (int pe = qwdev::plan_gemv(H->dev, H->num_sms, H->host_row_ptr.data())) {
-      if (pe == (int)cudaErrorInvalidConfiguration)
-        return fail(QW_ERR_UNSUPPORTED, "upload: layer too wide for the fused GEMV (at most 60 "
-                                        "chunks of 32 groups, i.e. about 30720 input channels)");
-      return cuda_fail((cudaError_t)pe, "gemv plan");
+      // the SIMT kernel cannot take the layer (more than 60 chunks of 32
+      // groups, or its x / 2-order rows / ring do not fit in shared memory):
+      // the tensor-core kernel K2m serves it, decided below
+      if (pe != (int)cudaErrorInvalidConfiguration) return cuda_fail((cudaError_t)pe, "gemv plan");
+      H->k2_ok = false;
     }
     {  // 2^-P so that 15 * max|scale2| * 2^-P lies in [2^14, 2^15): fp16 1st-order scales
       float mx = 0.0f;
@@ -447,7 +449,15 @@ int upload_packed(const qwb::PackedLayer& L, int device, uint32_t flags, qw_laye
     uint32_t ent_max = 0;
     for (uint32_t c = 0; c < gp.grid; ++c) ent_max = std::max(ent_max, gp.cta_e1[c] - gp.cta_e0[c]);
     const bool k2_slow = (L.csr.nnz() > 0 && !gp.csr_stage && ent_max > 1536) || (gp.kmax > 2 && !gp.wide) || !gp.xsm;
-    const bool want_mma = (flags & QW_UPLOAD_TENSOR_CORE) || (!(flags & QW_UPLOAD_SIMT) && k2_slow);
+    const bool want_mma = (flags & QW_UPLOAD_TENSOR_CORE) || (!(flags & QW_UPLOAD_SIMT) && (k2_slow || !H->k2_ok));
+    if (!H->k2_ok && !(H->dev.mg.ok && want_mma)) {
+      free_dev(H->dev);
+      return fail(QW_ERR_UNSUPPORTED, (flags & QW_UPLOAD_SIMT)
+                                          ? "upload: the SIMT batch-1 kernel cannot take this layer (more than 60 "
+                                            "chunks of 32 groups, or its shared-memory plan does not fit); "
+                                            "upload without QW_UPLOAD_SIMT"
+                                          : "upload: neither batch-1 kernel can take this layer");
+    }
     if (H->dev.mg.ok && want_mma) {
       std::vector<uint8_t> recs;
       qwb::repack_mma(L, H->dev.mg, H->dev.plan.s_scale, recs);
@@ -846,7 +856,7 @@ int qw_layer_clone(const qw_layer* L, qw_layer** out) {
   if (!L || !out) return fail(QW_ERR_ARG, "clone: null argument");
   cudaSetDevice(L->device);
   auto H = std::make_unique<qw_layer>();
-  H->device = L->device, H->num_sms = L->num_sms, H->info = L->info;
+  H->device = L->device, H->num_sms = L->num_sms, H->info = L->info, H->k2_ok = L->k2_ok;
   H->dev.g = L->dev.g;
   H->dev.plan = L->dev.plan;
   const auto& g = L->dev.g;
@@ -915,12 +925,16 @@ int qw_group_create(const qw_layer* const* layers, uint32_t n, qw_group** out) {
     }
     G->device = layers[0]->device;
     cudaSetDevice(G->device);
+    G->mma = true;
+    for (uint32_t i = 0; i < n; ++i) G->mma = G->mma && layers[i]->dev.mrecs != nullptr;
     const int e = qwdev::plan_gemv_group(G->plan, G->layers.data(), rps.data(), n, layers[0]->num_sms);
     if (e == (int)cudaErrorInvalidValue)
       return fail(QW_ERR_ARG, "group: layers must share cols, channel split and group2 (rows may differ)");
-    if (e) return cuda_fail((cudaError_t)e, "group plan");
-    G->mma = true;
-    for (uint32_t i = 0; i < n; ++i) G->mma = G->mma && layers[i]->dev.mrecs != nullptr;
+    if (e == (int)cudaErrorInvalidConfiguration && !G->mma)
+      return fail(QW_ERR_UNSUPPORTED, "group: the SIMT kernel's plan does not fit these layers (upload them with "
+                                      "the tensor-core kernel)");
+    if (e && e != (int)cudaErrorInvalidConfiguration) return cuda_fail((cudaError_t)e, "group plan");
+    if (e) G->plan.grid = 0;  // K2m group: the SIMT plan is never launched
     if (G->mma) {
       if (int me = qwdev::plan_mma(G->mplan, G->layers.data(), rps.data(), n, layers[0]->num_sms))
         return cuda_fail((cudaError_t)me, "group mma plan");
@@ -1072,6 +1086,10 @@ int qw_chain_create(const qw_chain_step* steps, uint32_t n, qw_chain** out) {
       *out = C.release();
       return (int)QW_OK;
     }
+    for (uint32_t s = 0; s < n; ++s)
+      for (uint32_t l = 0; l < steps[s].n; ++l)
+        if (!steps[s].layers[l]->k2_ok)
+          return fail(QW_ERR_UNSUPPORTED, "chain: a layer the SIMT kernel cannot take needs an all tensor-core chain");
     const int e = qwdev::plan_chain(&C->plan, d.data(), n, num_sms);
     if (e == (int)cudaErrorInvalidValue) return fail(QW_ERR_ARG, "chain: a step's layers differ in geometry");
     if (e == (int)cudaErrorNotSupported)

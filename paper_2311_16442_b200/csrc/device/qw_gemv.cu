@@ -805,9 +805,9 @@ namespace {
 
 // CTA ranges (one layer each) + shared-memory layout for the largest range
 int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_ptrs, const uint32_t* seg_rows,
-              uint32_t n, int num_sms) {
-  uint32_t per_sm = 1;
-  if (const char* e = qwdev::knob_str("QW_CTAS_PER_SM")) per_sm = std::max(1, std::atoi(e));
+              uint32_t n, int num_sms, uint32_t min_per_sm = 1) {
+  uint32_t per_sm = min_per_sm;
+  if (const char* e = qwdev::knob_str("QW_CTAS_PER_SM")) per_sm = std::max<uint32_t>(per_sm, std::atoi(e));
   uint64_t total = 0;
   uint32_t lq[kMaxSeg];
   for (uint32_t l = 0; l < n; ++l) lq[l] = (seg_rows[l] + kRowsPerQuad - 1) / kRowsPerQuad, total += lq[l];
@@ -965,12 +965,24 @@ int plan_ctas(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_pt
 }
 }  // namespace
 
+// one CTA per SM first; when the CTA's share does not fit in shared memory
+// (x, its 2-order rows -- one per row at group2 = 1 -- and a ring of at least
+// two slots) up to three CTAs per SM, each with a third of the rows, run in
+// waves
+int plan_ctas_fit(GemvPlan& p, const Geometry& G, const uint32_t* const* host_row_ptrs, const uint32_t* seg_rows,
+                  uint32_t n, int num_sms) {
+  int e = 0;
+  for (uint32_t f = 1; f <= 3; ++f)
+    if ((e = plan_ctas(p, G, host_row_ptrs, seg_rows, n, num_sms, f)) != (int)cudaErrorInvalidConfiguration) break;
+  return e;
+}
+
 int plan_gemv(DeviceLayer& L, int num_sms, const uint32_t* host_row_ptr) {
   GemvPlan& p = L.plan;
   if (int e = plan_geometry(p, L.g)) return e;
   const uint32_t* rp[1] = {host_row_ptr};
   const uint32_t rows[1] = {L.g.rows};
-  return plan_ctas(p, L.g, rp, rows, 1, num_sms);
+  return plan_ctas_fit(p, L.g, rp, rows, 1, num_sms);
 }
 
 int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_t* const* host_row_ptrs,
@@ -988,7 +1000,7 @@ int plan_gemv_group(GemvPlan& p, const DeviceLayer* const* layers, const uint32_
   p = layers[0]->plan;  // geometry part is identical
   uint32_t rows[kMaxSeg];
   for (uint32_t l = 0; l < n; ++l) rows[l] = layers[l]->g.rows;
-  return plan_ctas(p, G, host_row_ptrs, rows, n, num_sms);
+  return plan_ctas_fit(p, G, host_row_ptrs, rows, n, num_sms);
 }
 
 int launch_gemv_group(const GemvPlan& p, const DeviceLayer* const* layers, uint32_t n, const float* const* xs,

@@ -1,0 +1,80 @@
+"""Seeded random geometries through every device path against the f64
+oracle: 64 small (rows 1..700, any residue mod 4; cols a multiple of 16 up
+to 2560) and 16 large (rows up to 6000, cols up to 14336) layers,
+alpha 0 / 0.25 / 0.5 / 1 (pure 2-bit to pure 4-bit), group2 1..128 (row
+blocks that do and do not align with quads), outlier ratio 0..2 %.  Per case and
+batch-1 kernel (the default choice, K2 and K2m forced): batch 1 (rel-L2 and
+normwise max within the north-star 1e-2) and a column launch of a random
+batch (every column bit-identical to its batch-1 call); with the default
+upload the tcgen05 GEMM K4 at that batch (within 1e-2, deterministic run to
+run).  A layer K2's shared-memory plan cannot take is refused cleanly when
+K2 is forced and served by K2m by default."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2311_16442_b200 as qw
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def _cases(n=64, seed=2311, max_rows=700, max_cols16=160, first=0):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(first, first + n):
+        rows = int(rng.integers(1, max_rows + 1))
+        cols = 16 * int(rng.integers(1, max_cols16 + 1))
+        alpha = float(rng.choice([0.0, 0.25, 0.25, 0.5, 1.0]))
+        group2 = int(rng.choice([1, 3, 4, 5, 8, 16, 16, 32, 128]))
+        ratio = float(rng.choice([0.0, 0.001, 0.005, 0.01, 0.02]))
+        batch = int(rng.integers(2, 17))
+        out.append((i, rows, cols, alpha, group2, ratio, batch))
+    return out
+
+
+def _check(y, ref, what):
+    ref = np.asarray(ref, np.float64)
+    assert np.all(np.isfinite(y)), what
+    den = np.linalg.norm(ref)
+    err = float(np.linalg.norm(np.asarray(y, np.float64) - ref) / (den if den else 1.0))
+    assert err <= TOL, (what, err)
+    scale = np.max(np.abs(ref)) if ref.size else 0.0
+    assert np.max(np.abs(y - ref)) <= TOL * max(scale, 1e-30) + 1e-30, what
+
+
+# small layers (every residue, tails, tiny grids) and large ones (wide rows,
+# many CTAs, stream-K / split-K GEMM schedules)
+CASES = _cases() + _cases(n=16, seed=1644, max_rows=6000, max_cols16=896, first=64)
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "r{1}c{2}a{3}g{4}o{5}b{6}".format(*c))
+def test_random_geometry_all_paths(case):
+    import torch
+    i, rows, cols, alpha, group2, ratio, batch = case
+    layer = qw.synth_layer(rows, cols, seed=1000 + i, alpha=alpha, group2=group2, outlier_ratio=ratio)
+    xs = np.stack([qw.synth_activation(cols, 2000 + 17 * i + b) for b in range(batch)])
+    refs = [oracle.matvec_f64(layer, xs[b]) for b in range(batch)]
+    X = torch.from_numpy(xs).cuda()
+    for kernel in ("auto", "simt", "mma"):
+        try:
+            dl = qw.DeviceLayer(layer, kernel=kernel)
+        except qw.QWeightError as e:
+            # the SIMT kernel's shared-memory plan may not fit a wide layer:
+            # a clean refusal, and the default upload serves it with K2m
+            assert kernel == "simt" and e.status == 5, (kernel, str(e))
+            continue
+        y1 = dl.matvec(X[0].contiguous()).cpu().numpy()
+        _check(y1, refs[0], f"{kernel} batch 1")
+        yc = dl.matvec(X, batched="columns").cpu().numpy()
+        for b in range(batch):
+            yb = dl.matvec(X[b].contiguous()).cpu().numpy()
+            assert np.array_equal(yc[b].view(np.uint32), yb.view(np.uint32)), (kernel, "column launch", b)
+            _check(yc[b], refs[b], f"{kernel} column {b}")
+        if kernel == "auto" and dl.batched_path(batch, "gemm") == "gemm":
+            yg = dl.matvec(X, batched="gemm").cpu().numpy()
+            for b in range(batch):
+                _check(yg[b], refs[b], f"K4 column {b}")
+            assert np.array_equal(yg, dl.matvec(X, batched="gemm").cpu().numpy()), "K4 not deterministic"
+        dl.close()

@@ -74,12 +74,20 @@ GEOMS = [
 ]
 
 
-def test_too_wide_layer_is_rejected_cleanly():
-    """80 chunks of 32 groups exceed the fused kernel's 60: a clean QW_ERR_UNSUPPORTED."""
+def test_too_wide_layer_for_the_simt_kernel():
+    """80 chunks of 32 groups exceed the SIMT kernel's 60: forcing it is a
+    clean QW_ERR_UNSUPPORTED, and the default upload serves the layer with the
+    tensor-core kernel K2m, within the tolerance of the oracle."""
+    torch = _torch()
     layer = qw.synth_layer(16, 40960, seed=3, alpha=0.25, group2=16, outlier_ratio=0.002)
     with pytest.raises(qw.QWeightError) as ei:
-        qw.DeviceLayer(layer)
+        qw.DeviceLayer(layer, kernel="simt")
     assert ei.value.status == 5
+    dl = qw.DeviceLayer(layer)
+    assert dl.uses_tensor_core
+    x = qw.synth_activation(40960, 4)
+    y = dl.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert rel_l2(y, oracle.matvec_f64(layer, x)) <= TOL
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
