@@ -165,9 +165,12 @@ int qw_layer_upload(const qw_layer_view* view, int device, qw_layer** out);
  *     the measured shape sweep has the warp-MMA kernel
  *     K2m ahead -- layers whose outliers do not fit K2's shared-memory CSR
  *     stage (K2 then falls back to a global-memory CSR loop) and layers
- *     wider than K2's two-groups-per-lane limit (70B down_proj);
+ *     wider than K2's two-groups-per-lane limit (70B down_proj), and
+ *     layers K2 cannot take at all (more than 60 chunks of 32 groups, or x +
+ *     2-order rows + a two-slot ring beyond shared memory even at three CTAs
+ *     per SM);
  *   QW_UPLOAD_TENSOR_CORE: always K2m (16-row tile format, qw_mma.cu);
- *   QW_UPLOAD_SIMT: always K2.
+ *   QW_UPLOAD_SIMT: always K2 (QW_ERR_UNSUPPORTED where K2 cannot take it).
  * Layers whose group2 is not a multiple of 16 always keep K2. */
 #define QW_UPLOAD_TENSOR_CORE 1u
 #define QW_UPLOAD_SIMT 2u
