@@ -8,7 +8,10 @@ normwise max within the north-star 1e-2) and a column launch of a random
 batch (every column bit-identical to its batch-1 call); with the default
 upload the tcgen05 GEMM K4 at that batch (within 1e-2, deterministic run to
 run).  A layer K2's shared-memory plan cannot take is refused cleanly when
-K2 is forced and served by K2m by default."""
+K2 is forced and served by K2m by default.  Also 24 random layer groups
+(GQA-style differing rows, batch 1..8, each output bit-identical to the
+layer's own launch) and 16 random tensor-parallel shardings (column / row
+split over 2..8 ranks, exchange completed on the host)."""
 import numpy as np
 import pytest
 
@@ -78,3 +81,97 @@ def test_random_geometry_all_paths(case):
                 _check(yg[b], refs[b], f"K4 column {b}")
             assert np.array_equal(yg, dl.matvec(X, batched="gemm").cpu().numpy()), "K4 not deterministic"
         dl.close()
+
+
+def _group_cases(n=24, seed=77):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        cols = 16 * int(rng.integers(1, 257))
+        nl = int(rng.integers(2, 4))
+        rows = [int(rng.integers(1, 1500)) for _ in range(nl)]
+        alpha = float(rng.choice([0.0, 0.25, 0.5, 1.0]))
+        group2 = int(rng.choice([3, 4, 16, 16, 32]))
+        ratio = float(rng.choice([0.0, 0.002, 0.01]))
+        batch = int(rng.integers(1, 9))
+        kernel = str(rng.choice(["auto", "simt", "mma"]))
+        out.append((i, cols, tuple(rows), alpha, group2, ratio, batch, kernel))
+    return out
+
+
+@pytest.mark.parametrize("case", _group_cases(), ids=lambda c: "c{1}r{2}a{3}g{4}o{5}b{6}{7}".format(*c))
+def test_random_layer_group(case):
+    """A layer group (GQA-style: the row counts differ) at batch 1 or a batch:
+    every output bit-identical to the layer's own launch and within 1e-2 of
+    the oracle."""
+    import torch
+    i, cols, rows, alpha, group2, ratio, batch, kernel = case
+    # one channel split for the group: the same calibration vector for every layer
+    h = qw.synth_calibration(cols, 900 + i)
+    layers = [qw.quantize_layer(qw.synth_gaussian(r, cols, 600 + 10 * i + j), h, alpha, group2, ratio)
+              for j, r in enumerate(rows)]
+    try:
+        dls = [qw.DeviceLayer(L, kernel=kernel) for L in layers]
+    except qw.QWeightError as e:
+        assert kernel == "simt" and e.status == 5, str(e)
+        return
+    grp = qw.LayerGroup(dls)
+    xs = np.stack([qw.synth_activation(cols, 3000 + 13 * i + b) for b in range(batch)])
+    X = torch.from_numpy(xs).cuda()
+    x_in = X[0].contiguous() if batch == 1 else X
+    outs = [o.cpu().numpy().reshape(batch, -1) for o in grp.matvec(x_in)]
+    for L, dl, o in zip(layers, dls, outs):
+        own = dl.matvec(x_in).cpu().numpy().reshape(batch, -1) if batch == 1 else None
+        for b in range(batch):
+            ref = oracle.matvec_f64(L, xs[b])
+            _check(o[b], ref, f"group layer rows {L.cfg.rows} column {b}")
+            yb = dl.matvec(X[b].contiguous()).cpu().numpy()
+            assert np.array_equal(o[b].view(np.uint32), yb.view(np.uint32)), ("group vs own launch", b)
+        if own is not None:
+            assert np.array_equal(own, o)
+    grp.close()
+
+
+def _tp_cases(n=16, seed=99):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        world = int(rng.integers(2, 9))
+        mode = str(rng.choice(["col", "row"]))
+        rows = int(rng.integers(world * 16, 3000))
+        cols = 48 * int(rng.integers(world, 80))  # whole triples: paired tiles for the row split
+        group2 = int(rng.choice([4, 16, 16, 32]))
+        ratio = float(rng.choice([0.0, 0.002, 0.01]))
+        out.append((i, world, mode, rows, cols, group2, ratio))
+    return out
+
+
+@pytest.mark.parametrize("case", _tp_cases(), ids=lambda c: "w{1}{2}r{3}c{4}g{5}o{6}".format(*c))
+def test_random_tensor_parallel_shards(case):
+    """Quantize once, shard (column split: row ranges on 2-order block
+    boundaries; row split: whole tile pairs), run every shard's GPU matvec and
+    complete the exchange on the host (concatenate / sum in rank order): the
+    result is within 1e-2 of the unsharded layer's f64 oracle."""
+    import torch
+
+    from paper_2311_16442_b200.tp import shard_layer
+    i, world, mode, rows, cols, group2, ratio = case
+    layer = qw.synth_layer(rows, cols, seed=700 + i, alpha=0.25, group2=group2, outlier_ratio=ratio)
+    if mode == "row" and (layer.cfg.tail2_blocks or layer.cfg.tail4_blocks):
+        pytest.skip("row split needs paired tiles")
+    x = qw.synth_activation(cols, 800 + i)
+    ref = oracle.matvec_f64(layer, x)
+    parts = []
+    for r in range(world):
+        shard, ranges, idx = shard_layer(layer, r, world, mode)
+        xs = x if mode == "col" else np.where(idx >= 0, x[np.maximum(idx, 0)], 0.0).astype(np.float32)
+        y = qw.DeviceLayer(shard).matvec(torch.from_numpy(np.ascontiguousarray(xs)).cuda()).cpu().numpy()
+        parts.append(y)
+    if mode == "col":
+        got = np.concatenate(parts)
+    else:
+        got = parts[0].astype(np.float32).copy()
+        for p in parts[1:]:
+            got += p
+    assert got.shape == ref.shape
+    _check(got, ref, f"{mode} split over {world}")
