@@ -175,3 +175,37 @@ def test_random_tensor_parallel_shards(case):
             got += p
     assert got.shape == ref.shape
     _check(got, ref, f"{mode} split over {world}")
+
+
+def _producer_cases(n=24, seed=5):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        rows = int(rng.integers(1, 1200))
+        cols = 16 * int(rng.integers(1, 200))
+        alpha = float(rng.choice([0.0, 0.125, 0.25, 0.5, 0.75, 1.0]))
+        group2 = int(rng.choice([1, 2, 3, 5, 8, 16, 64, 128]))
+        ratio = float(rng.choice([0.0, 0.0005, 0.002, 0.01, 0.05]))
+        ties = bool(rng.integers(0, 2))
+        out.append((i, rows, cols, alpha, group2, ratio, ties))
+    return out
+
+
+@pytest.mark.parametrize("case", _producer_cases(), ids=lambda c: "r{1}c{2}a{3}g{4}o{5}t{6}".format(*c))
+def test_random_device_producer_bit_identical(case, tmp_path):
+    """qw_device_quantize vs the CPU producer (itself pinned to the
+    reference) on random shapes, as serialized QWL1 bytes; half the cases
+    plant equal-magnitude outliers to exercise the top-K tie-break."""
+    i, rows, cols, alpha, group2, ratio, ties = case
+    w = qw.synth_gaussian(rows, cols, 4000 + i)
+    if ties:
+        rng = np.random.default_rng(i)
+        for _ in range(min(8, rows * cols // 4)):
+            w[int(rng.integers(0, rows)), int(rng.integers(0, cols))] = 7.5  # exact ties in |w|
+    h = qw.synth_calibration(cols, 4100 + i)
+    cpu = qw.quantize_layer(w, h, alpha, group2, ratio)
+    gpu = qw.quantize_layer_gpu(w, h, alpha, group2, ratio)
+    pc, pg = tmp_path / "cpu.qwl", tmp_path / "gpu.qwl"
+    qw.write_packed_layer(cpu, str(pc))
+    qw.write_packed_layer(gpu, str(pg))
+    assert pg.read_bytes() == pc.read_bytes()
