@@ -11,7 +11,9 @@ run).  A layer K2's shared-memory plan cannot take is refused cleanly when
 K2 is forced and served by K2m by default.  Also 24 random layer groups
 (GQA-style differing rows, batch 1..8, each output bit-identical to the
 layer's own launch) and 16 random tensor-parallel shardings (column / row
-split over 2..8 ranks, exchange completed on the host)."""
+split over 2..8 ranks, exchange completed on the host), 24 random shapes
+through the GPU producer (QWL1 bytes identical to the CPU producer's) and 16
+random tcgen05 geometries for the A-tile exactness."""
 import numpy as np
 import pytest
 
@@ -209,3 +211,53 @@ def test_random_device_producer_bit_identical(case, tmp_path):
     qw.write_packed_layer(cpu, str(pc))
     qw.write_packed_layer(gpu, str(pg))
     assert pg.read_bytes() == pc.read_bytes()
+
+
+def _a_tile_cases(n=16, seed=11):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        rows = int(rng.integers(1, 2000))
+        cols = 128 * int(rng.integers(1, 40))
+        group2 = int(rng.choice([4, 8, 16, 16, 32, 128]))
+        ratio = float(rng.choice([0.0, 0.002, 0.01]))
+        out.append((i, rows, cols, group2, ratio))
+    return out
+
+
+@pytest.mark.parametrize("case", _a_tile_cases(), ids=lambda c: "r{1}c{2}g{3}o{4}".format(*c))
+def test_random_k4_a_tile_exactness(case):
+    """SURVEY §8(c)(2) on random K4 geometries: with a one-hot activation at
+    permuted slot k, column n of the batched GEMM equals
+    RN_fp16(w[:, k] 2^-P) 2^P plus the slot's CSR outliers, bit for bit
+    (tests/test_gpu_parity.py states the argument)."""
+    import ctypes as C
+
+    import torch
+    i, rows, cols, group2, ratio = case
+    layer = qw.synth_layer(rows, cols, seed=5000 + i, group2=group2, outlier_ratio=ratio)
+    dl = qw.DeviceLayer(layer)
+    if dl.batched_path(8, "gemm") != "gemm":
+        pytest.skip("geometry not on the tcgen05 path (unpaired tiles)")
+    P = C.c_int()
+    assert qw.lib().qw_debug_gemm_shift(dl._h, C.byref(P)) == 0
+    w = oracle.reconstruct_dense(layer)
+    perm = layer.plan_perm.astype(np.int64)
+    real = np.nonzero(perm != qw.PAD)[0]
+    rng = np.random.default_rng(6000 + i)
+    slots = rng.choice(real, min(8, real.size), replace=False)
+    xs = np.zeros((len(slots), cols), np.float32)
+    for n, k in enumerate(slots):
+        xs[n, perm[k]] = 1.0
+    Y = dl.matvec(torch.from_numpy(xs).cuda(), batched="gemm").cpu().numpy()
+    rp, ci = layer.row_ptr.astype(np.int64), layer.col_ind.astype(np.int64)
+    vals = layer.values.view(np.float16).astype(np.float32)
+    scale = np.float32(2.0) ** np.float32(P.value)
+    for n, k in enumerate(slots):
+        a = (w[:, k] / scale).astype(np.float16).astype(np.float32) * scale
+        csr = np.zeros(rows, np.float32)
+        for r in range(rows):
+            hit = np.nonzero(ci[rp[r]:rp[r + 1]] == k)[0]
+            if hit.size:
+                csr[r] = vals[rp[r] + hit[0]]
+        assert np.array_equal(Y[n].view(np.uint32), (a + csr).view(np.uint32)), (n, int(k))
