@@ -219,6 +219,32 @@ def test_tp_peer_exchange_fused_with_the_gemv(world, rows, cols, mode):
             assert np.array_equal(ys[r], ys[0])
 
 
+def _peer_fuzz_cases(n=8, seed=31):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        world = int(rng.integers(2, 7))
+        out.append((world, int(rng.integers(world * 16, 2500)), 48 * int(rng.integers(world, 90)),
+                    int(rng.choice([4, 16, 32])), str(rng.choice(["col", "row"]))))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,rows,cols,g2,mode", _peer_fuzz_cases())
+def test_tp_peer_exchange_random_geometries(world, rows, cols, g2, mode):
+    """The fused peer exchange on seeded random shapes, world sizes and
+    2-order group sizes (ranks as streams of one process)."""
+    layer = qw.synth_layer(rows, cols, seed=rows * 7 + cols, group2=g2, outlier_ratio=0.005)
+    if mode == "row" and (layer.cfg.tail2_blocks or layer.cfg.tail4_blocks):
+        pytest.skip("row split needs paired tiles")
+    x = qw.synth_activation(cols, rows)
+    ys = _peer_ranks_in_one_process(layer, world, mode, x)
+    ref = oracle.matvec_f64(layer, x)
+    for r in range(world):
+        assert float(np.linalg.norm(ys[r] - ref) / np.linalg.norm(ref)) <= 1e-2, r
+        assert np.array_equal(ys[r], ys[0])
+
+
 def _ipc_worker(rank, port, q):
     """Rank 1 maps rank 0's buffer through its CUDA IPC handle and writes into
     it (qw_peer_reduce with one slot); rank 0 reads the values back."""
