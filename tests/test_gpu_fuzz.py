@@ -13,7 +13,8 @@ K2 is forced and served by K2m by default.  Also 24 random layer groups
 layer's own launch) and 16 random tensor-parallel shardings (column / row
 split over 2..8 ranks, exchange completed on the host), 24 random shapes
 through the GPU producer (QWL1 bytes identical to the CPU producer's) and 16
-random tcgen05 geometries for the A-tile exactness."""
+random tcgen05 geometries for the A-tile exactness, and 12 random
+persistent decode chains (dependent steps, K2 and K2m chain kernels)."""
 import numpy as np
 import pytest
 
@@ -261,3 +262,59 @@ def test_random_k4_a_tile_exactness(case):
             if hit.size:
                 csr[r] = vals[rp[r] + hit[0]]
         assert np.array_equal(Y[n].view(np.uint32), (a + csr).view(np.uint32)), (n, int(k))
+
+
+def _chain_cases(n=12, seed=21):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        steps = int(rng.integers(2, 6))
+        dims = [16 * int(rng.integers(4, 200)) for _ in range(steps + 1)]  # x width of each step, then the last y
+        extra = [int(rng.integers(0, 3)) for _ in range(steps)]           # more layers reading the same x
+        kernel = str(rng.choice(["simt", "mma"]))
+        out.append((i, tuple(dims), tuple(extra), kernel))
+    return out
+
+
+@pytest.mark.parametrize("case", _chain_cases(), ids=lambda c: "d{1}e{2}{3}".format(*c).replace(" ", ""))
+def test_random_decode_chain(case):
+    """The persistent chain kernel (DecodeChain) over random dependent steps:
+    step s reads the output of step s-1's first layer; every output within
+    1e-2 of the oracle applied to the chain's own input of that step, and run
+    to run deterministic."""
+    import torch
+    i, dims, extra, kernel = case
+    steps, keep = [], []
+    x0 = torch.from_numpy(qw.synth_activation(dims[0], 7000 + i)).cuda()
+    x = x0
+    for s in range(len(dims) - 1):
+        cols = dims[s]
+        # the SIMT chain kernel takes one geometry per step, the K2m one differing rows (GQA)
+        rows = [dims[s + 1]] + [dims[s + 1] if kernel == "simt" else 16 * (1 + (s + j) % 5)
+                                for j in range(extra[s])]
+        h = qw.synth_calibration(cols, 7100 + 10 * i + s)
+        layers = [qw.quantize_layer(qw.synth_gaussian(r, cols, 7200 + 100 * i + 10 * s + j), h, 0.25, 16, 0.005)
+                  for j, r in enumerate(rows)]
+        dls = [qw.DeviceLayer(L, kernel=kernel) for L in layers]
+        ys = [torch.empty(r, device="cuda") for r in rows]
+        steps.append((dls, x, ys, s > 0))
+        keep.append((layers, x, ys))
+        x = ys[0]
+    try:
+        chain = qw.DecodeChain(steps)
+    except qw.QWeightError as e:
+        assert e.status == 5, str(e)  # a geometry the chain kernel does not cover: refused cleanly
+        pytest.skip(str(e))
+    chain.run()
+    torch.cuda.synchronize()
+    first = [[y.cpu().numpy().copy() for y in ys] for _, _, ys in keep]
+    for s, (layers, xin, ys) in enumerate(keep):
+        xv = xin.cpu().numpy()
+        for L, y in zip(layers, ys):
+            _check(y.cpu().numpy(), oracle.matvec_f64(L, xv), f"chain step {s}")
+    chain.run()
+    torch.cuda.synchronize()
+    for s, (_, _, ys) in enumerate(keep):
+        for a, y in zip(first[s], ys):
+            assert np.array_equal(a, y.cpu().numpy()), ("chain not deterministic", s)
+    chain.close()
