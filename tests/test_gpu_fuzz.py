@@ -14,7 +14,8 @@ layer's own launch) and 16 random tensor-parallel shardings (column / row
 split over 2..8 ranks, exchange completed on the host), 24 random shapes
 through the GPU producer (QWL1 bytes identical to the CPU producer's) and 16
 random tcgen05 geometries for the A-tile exactness, and 12 random
-persistent decode chains (dependent steps, K2 and K2m chain kernels)."""
+persistent decode chains (dependent steps, K2 and K2m chain kernels) and 8
+random back-to-back PDL chains (bit-identical to synchronised calls)."""
 import numpy as np
 import pytest
 
@@ -318,3 +319,33 @@ def test_random_decode_chain(case):
         for a, y in zip(first[s], ys):
             assert np.array_equal(a, y.cpu().numpy()), ("chain not deterministic", s)
     chain.close()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_pdl_chains_match_synchronised_calls(seed):
+    """Back-to-back dependent launches with programmatic dependent launch
+    (each call reads the previous call's y; the next kernel starts under the
+    previous one and waits in griddepcontrol.wait) on random shapes, batch 1
+    and batched (column launches / K4), K2 and K2m: bit-identical to the same
+    calls with a device synchronisation between them."""
+    import torch
+    rng = np.random.default_rng(8800 + seed)
+    kernel = str(rng.choice(["simt", "mma", "auto"]))
+    batch = int(rng.choice([1, 1, 3, 8]))
+    dims = [16 * int(rng.integers(8, 300)) for _ in range(6)]
+    dls = [qw.DeviceLayer(qw.synth_layer(dims[s + 1], dims[s], seed=8900 + 10 * seed + s, outlier_ratio=0.005),
+                          kernel=kernel) for s in range(5)]
+    x0 = np.stack([qw.synth_activation(dims[0], 9000 + seed + b) for b in range(batch)])
+    X0 = torch.from_numpy(x0 if batch > 1 else x0[0]).cuda()
+    ref, x = [], X0
+    for d in dls:  # synchronised
+        x = d.matvec(x)
+        torch.cuda.synchronize()
+        ref.append(x.cpu().numpy())
+    got, x = [], X0
+    for d in dls:  # back to back under PDL
+        x = d.matvec(x, pdl=True)
+        got.append(x)
+    torch.cuda.synchronize()
+    for s in range(5):
+        assert np.array_equal(got[s].cpu().numpy(), ref[s]), (kernel, batch, s)
