@@ -86,6 +86,13 @@ def main():
     xs = torch.from_numpy(np.stack([qw.synth_activation(2048, 60 + i) for i in range(3)])).cuda()
     step("10240x2048 K4 stream-K b=3", lambda: dl.matvec(xs, batched="gemm"))
     dl.close()
+    # a wide layer at group2 = 1 (a 2-order row per row): K2's plan needs
+    # three CTAs per SM (run in waves)
+    layer = qw.synth_layer(1200, 13792, seed=5, group2=1, outlier_ratio=0.005)
+    dl = qw.DeviceLayer(layer, kernel="simt")
+    xw = torch.from_numpy(qw.synth_activation(13792, 5)).cuda()
+    step("1200x13792 g2=1 K2 (several CTAs per SM)", lambda: dl.matvec(xw))
+    dl.close()
     # a layer group (one launch for three layers sharing x)
     layers = [qw.DeviceLayer(qw.synth_layer(r, 1024, seed=r, outlier_ratio=0.005)) for r in (256, 128, 128)]
     grp = qw.LayerGroup(layers)
