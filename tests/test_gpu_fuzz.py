@@ -1,6 +1,7 @@
 """Seeded random geometries through every device path against the f64
 oracle: 64 small (rows 1..700, any residue mod 4; cols a multiple of 16 up
-to 2560) and 16 large (rows up to 6000, cols up to 14336) layers,
+to 2560), 16 large (rows up to 6000, cols up to 14336) and 8 very wide
+(cols 16384..30720: x gathered from global memory) layers,
 alpha 0 / 0.25 / 0.5 / 1 (pure 2-bit to pure 4-bit), group2 1..128 (row
 blocks that do and do not align with quads), outlier ratio 0..2 %.  Per case and
 batch-1 kernel (the default choice, K2 and K2m forced): batch 1 (rel-L2 and
@@ -53,7 +54,9 @@ def _check(y, ref, what):
 
 # small layers (every residue, tails, tiny grids) and large ones (wide rows,
 # many CTAs, stream-K / split-K GEMM schedules)
-CASES = _cases() + _cases(n=16, seed=1644, max_rows=6000, max_cols16=896, first=64)
+CASES = (_cases() + _cases(n=16, seed=1644, max_rows=6000, max_cols16=896, first=64) +
+         # wider than the 16384 channels K2 stages in shared memory (x gathered from global memory)
+         [c for c in _cases(n=40, seed=4242, max_rows=300, max_cols16=1920, first=80) if c[2] > 16384][:8])
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "r{1}c{2}a{3}g{4}o{5}b{6}".format(*c))
