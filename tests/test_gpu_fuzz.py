@@ -16,7 +16,8 @@ split over 2..8 ranks, exchange completed on the host), 24 random shapes
 through the GPU producer (QWL1 bytes identical to the CPU producer's) and 16
 random tcgen05 geometries for the A-tile exactness, and 12 random
 persistent decode chains (dependent steps, K2 and K2m chain kernels) and 8
-random back-to-back PDL chains (bit-identical to synchronised calls)."""
+random back-to-back PDL chains (bit-identical to synchronised calls) and 8
+random layers loaded straight from QWL1 containers."""
 import numpy as np
 import pytest
 
@@ -352,3 +353,21 @@ def test_random_pdl_chains_match_synchronised_calls(seed):
     torch.cuda.synchronize()
     for s in range(5):
         assert np.array_equal(got[s].cpu().numpy(), ref[s]), (kernel, batch, s)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_qwl_straight_to_device(seed, tmp_path):
+    """A random layer written as a QWL1 container and loaded straight into
+    HBM (qw_layer_load / qw_layer_upload_qwl: parse, CRC, validate, repack)
+    computes the same y, bit for bit, as the in-memory upload."""
+    import torch
+    rng = np.random.default_rng(9500 + seed)
+    rows, cols = int(rng.integers(1, 3000)), 16 * int(rng.integers(1, 600))
+    layer = qw.synth_layer(rows, cols, seed=9600 + seed, alpha=float(rng.choice([0.0, 0.25, 1.0])),
+                           group2=int(rng.choice([1, 5, 16, 128])), outlier_ratio=float(rng.choice([0.0, 0.005])))
+    path = tmp_path / "layer.qwl"
+    qw.write_packed_layer(layer, str(path))
+    x = torch.from_numpy(qw.synth_activation(cols, seed)).cuda()
+    y = qw.DeviceLayer(layer).matvec(x).cpu().numpy()
+    for dl in (qw.DeviceLayer.load(str(path)), qw.DeviceLayer.from_qwl_bytes(path.read_bytes())):
+        assert np.array_equal(dl.matvec(x).cpu().numpy().view(np.uint32), y.view(np.uint32))
