@@ -515,13 +515,12 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
       if (a.wait_x) pdl_wait();  // x is the previous kernel's output
       xs = g_x;
     }
-    // Two teams need the same X: team 0 prepares it and hands it to team 1
-    // through team 1's (not yet used) reduction windows.
+    // Each team gathers and scales its own X (the same values: handing team
+    // 0's X to team 1 through shared memory put a barrier over both teams in
+    // front of the main loop, 2 % slower on the bench step).
     half2 X[KG][16], nsxh[KG];
     float yscale;
-    const bool share = TM && KG == 1 && T == 2;
-    uint32_t* xsh = reinterpret_cast<uint32_t*>(smem + a.win_off) + (W + wt) * kWinWords + lane * 20u;
-    if (!share || team == 0) {
+    {
     const uint32_t n2 = G.cols - G.n4;
     float xv[KG][16];
     float mx = 0.0f;
@@ -581,29 +580,6 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     }
     // every accumulated term is in units of 2^(sh + 24) (and 2^P for 2-bit s1)
     yscale = pow2f(max(-126, min(127, sh + 24))) * (TWO ? 1.0f / s_scale : 1.0f);
-    if (share) {
-      uint4* d = reinterpret_cast<uint4*>(xsh);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        d[q] = make_uint4(*reinterpret_cast<uint32_t*>(&X[0][4 * q]), *reinterpret_cast<uint32_t*>(&X[0][4 * q + 1]),
-                          *reinterpret_cast<uint32_t*>(&X[0][4 * q + 2]), *reinterpret_cast<uint32_t*>(&X[0][4 * q + 3]));
-      d[4] = make_uint4(*reinterpret_cast<uint32_t*>(&nsxh[0]), __float_as_uint(yscale), 0u, 0u);
-    }
-    }
-    if (share) {
-      named_sync(3, 2 * W * 32);
-      if (team == 1) {
-        const uint4* d = reinterpret_cast<const uint4*>(xsh);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint4 v = d[q];
-          X[0][4 * q] = as_h2(v.x), X[0][4 * q + 1] = as_h2(v.y), X[0][4 * q + 2] = as_h2(v.z),
-          X[0][4 * q + 3] = as_h2(v.w);
-        }
-        const uint4 v = d[4];
-        nsxh[0] = as_h2(v.x), yscale = __uint_as_float(v.y);
-        __syncwarp();  // every lane has read before the window is reused
-      }
     }
     if (threadIdx.x == 0) stamp(a.dbg, 2);  // prologue done
     if (threadIdx.x == 0 && a.dbg && nunit) {  // diagnostics: the first unit is in
