@@ -704,12 +704,16 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
 
 using GemvFn = void (*)(GemvArgs);
 
+// quads per ring slot of a one-group-per-lane kernel: 2, or 4 (diagnostics);
+// the plan (quads_per_slot) and the instantiation (pick2) both read it here
+uint32_t nq1() { return env_u32("QW_NQ1", 2) == 4 ? 4u : 2u; }
+
 template <bool UNI, bool XSM, bool PEER = false>
 GemvFn pick2(uint32_t kg) {
   switch (kg) {
     case 1:
-      if (UNI && env_u32("QW_NQ1", 2) == 2) return gemv_kernel<1, 2, UNI, XSM, false, PEER>;
-      return gemv_kernel<1, UNI ? 4 : 1, UNI, XSM, false, PEER>;
+      if (!UNI) return gemv_kernel<1, 1, UNI, XSM, false, PEER>;
+      return nq1() == 2 ? gemv_kernel<1, 2, UNI, XSM, false, PEER> : gemv_kernel<1, UNI ? 4 : 1, UNI, XSM, false, PEER>;
     case 2: return gemv_kernel<2, UNI ? 2 : 1, UNI, XSM, false, PEER>;
     case 3: return gemv_kernel<3, 1, UNI, XSM, false, PEER>;
     default: return gemv_kernel<4, 1, UNI, XSM, false, PEER>;
@@ -728,7 +732,7 @@ GemvFn pick_peer(uint32_t kg, bool xsm, bool teams) {
   return teams ? pick_teams<true>(kg) : (xsm ? pick2<true, true, true>(kg) : pick2<true, false, true>(kg));
 }
 uint32_t quads_per_slot(uint32_t kg, bool uni) {
-  return !uni ? 1u : (kg == 1 ? env_u32("QW_NQ1", 2) : (kg == 2 ? 2u : 1u));
+  return !uni ? 1u : (kg == 1 ? nq1() : (kg == 2 ? 2u : 1u));
 }
 
 cudaError_t launch_ex(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
