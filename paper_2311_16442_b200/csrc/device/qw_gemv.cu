@@ -419,8 +419,16 @@ __global__ void __launch_bounds__(TM ? 576 : (KG <= 2 ? 320 : 544), (TM || KG > 
     auto scales_of = [&](const uint8_t* sb, int j, int k, uint32_t u) -> uint2 {
       const uint32_t r0 = (q0 + u * NQ + j) * kRowsPerQuad;
       if (!UNI || r0 >= rb_end[j]) {
-        load_scales(j, r0);
-        rb_end[j] = (row_block(r0) + 1) * G.group2;
+        if (UNI && j > 0 && r0 < rb_end[j > 0 ? j - 1 : 0]) {
+          // the unit's previous quad is in the same 2-order row block (loaded
+          // just now): its scales, no second decode
+#pragma unroll
+          for (int kk = 0; kk < KG; ++kk) A2[j][kk][0] = A2[j - 1][kk][0], C2[j][kk][0] = C2[j - 1][kk][0];
+          rb_end[j] = rb_end[j - 1];
+        } else {
+          load_scales(j, r0);
+          rb_end[j] = (row_block(r0) + 1) * G.group2;
+        }
       }
       const uint2 m = *reinterpret_cast<const uint2*>(sb + j * dense + off_p[k]);
       const int i1 = UNI ? 0 : 1;
