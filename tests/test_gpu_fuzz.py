@@ -18,6 +18,8 @@ random tcgen05 geometries for the A-tile exactness, and 12 random
 persistent decode chains (dependent steps, K2 and K2m chain kernels) and 8
 random back-to-back PDL chains (bit-identical to synchronised calls) and 8
 random layers loaded straight from QWL1 containers."""
+import os
+
 import numpy as np
 import pytest
 
@@ -55,9 +57,11 @@ def _check(y, ref, what):
 
 # small layers (every residue, tails, tiny grids) and large ones (wide rows,
 # many CTAs, stream-K / split-K GEMM schedules)
-CASES = (_cases() + _cases(n=16, seed=1644, max_rows=6000, max_cols16=896, first=64) +
+# QW_FUZZ_N / QW_FUZZ_SEED: a longer or different draw of the small layers (stress runs)
+_N, _SEED = int(os.environ.get("QW_FUZZ_N", "64")), int(os.environ.get("QW_FUZZ_SEED", "2311"))
+CASES = (_cases(n=_N, seed=_SEED) + _cases(n=16, seed=1644, max_rows=6000, max_cols16=896, first=_N) +
          # wider than the 16384 channels K2 stages in shared memory (x gathered from global memory)
-         [c for c in _cases(n=40, seed=4242, max_rows=300, max_cols16=1920, first=80) if c[2] > 16384][:8])
+         [c for c in _cases(n=40, seed=4242, max_rows=300, max_cols16=1920, first=_N + 16) if c[2] > 16384][:8])
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "r{1}c{2}a{3}g{4}o{5}b{6}".format(*c))
